@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: effective conductivity of a 512^3 random-inclusion
+RVE (reference RANDOM_BALL_PRESETS["a"] geometry, contrast 100) in all three
+load directions, PCG to relative residual 1e-6 (BASELINE.json config 4).
+
+One "step" = the full three-direction homogenization (3 x homogenize():
+permute + scale + stats + LP + preconditioner setup + rhs + PCG + flux),
+inputs resident in HBM.  Prints ONE JSON line (rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference times the reference algorithm's CPU implementation (the
+numpy oracle port, oracle/etc_oracle.py) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "PCG time-to-solution, 512^3 random-inclusion RVE (contrast 100), x/y/z, rtol 1e-6"
+KCLASS = ["stencil", "update_xdct", "ydct", "zsolve", "ydct_inv", "xdct_inv", "setup"]
+
+
+def bytes_per_cell(iso: bool) -> dict:
+    """Algorithmic (compulsory) HBM bytes per cell per launch, f64."""
+    return {
+        "stencil": 40 if iso else 56,  # z, w_old, s(x3) read; w_new, q written
+        "update_xdct": 56,  # p, w, r, q read; p, r, t written
+        "ydct": 16, "zsolve": 16, "ydct_inv": 16, "xdct_inv": 16,
+    }
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"etc_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        try:
+            self.path.unlink()
+        except OSError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline: the oracle port of the reference algorithm (numpy + pocketfft)
+# ----------------------------------------------------------------------------
+
+def cpu_sample(n: int, contrast: float, iters: int, workers: int) -> dict:
+    """Setup and per-PCG-iteration host time of the reference algorithm at n^3
+    (oracle/etc_oracle.py: same stencil, Makhoul DCT via pocketfft, Thomas
+    sweep, Alg. 1 vector algebra), z direction."""
+    from oracle import etc_oracle as O
+
+    k = O.random_balls(n, 40, 0.05, 0.15, contrast, 11)
+    t0 = time.perf_counter()
+    s = O.scale(k, 1.0 / n)
+    fc = O.faces(s, s, s)
+    refs = O.reference_constants(O.stats(fc))
+    tab = O.tables(n, n, n, refs)
+    b = O.rhs(fc, k.shape, 1.0, 0.0).reshape(-1)
+    t_setup = time.perf_counter() - t0
+    shape = k.shape
+    A = lambda u: O.stencil(fc, u.reshape(shape)).reshape(-1)
+    M = lambda r: O.precond(tab, r.reshape(shape), workers).reshape(-1)
+    r = b.copy()
+    p = np.zeros_like(b)
+    z = M(r)
+    w = z.copy()
+    rho = float(np.dot(r, z))
+    times = []
+    for _ in range(iters):
+        t0 = time.perf_counter()
+        q = A(w)
+        qw = float(np.dot(q, w))
+        _ = 100 * 2.2e-16 * float(np.linalg.norm(q)) * float(np.linalg.norm(w))
+        alpha = rho / qw
+        p += alpha * w
+        r -= alpha * q
+        _ = float(np.linalg.norm(r))
+        z = M(r)
+        rho_new = float(np.dot(r, z))
+        w = z + (rho_new / rho) * w
+        rho = rho_new
+        times.append(time.perf_counter() - t0)
+    return {"setup_s": t_setup, "iter_s": min(times), "iters": iters}
+
+
+def iterations_512() -> dict:
+    """Reference iteration counts at 512^3 (tests/golden/solves_512.json, made
+    by running the reference here), else None per missing axis."""
+    out = {}
+    p = ROOT / "tests" / "golden" / "solves_512.json"
+    if p.exists():
+        for c in json.loads(p.read_text()):
+            out[c["axis"]] = int(c["iterations"])
+    return out
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+
+    import paper_2404_02433_b200 as P
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = world > 1
+    if dist:
+        import torch.distributed as td
+    n = args.n
+    field = P.gen_random_balls(n, 40, 0.05, 0.15, args.contrast, 11, device=dev)
+    axes = args.axes
+
+    def step():
+        return P.effective_tensor(field, rtol=args.rtol, axes=axes, device=dev)
+
+    for _ in range(args.warmup):
+        kappa, reps = step()
+    torch.cuda.synchronize()
+    plan = P.get_plan(field.grid, dev)
+    lib = plan.lib
+    import ctypes as C
+
+    ms8 = (C.c_double * 8)()
+    cnt8 = (C.c_longlong * 8)()
+    lib.etc_profile_read(plan.handle, ms8, cnt8, 1)  # reset counters
+
+    clocks = Clocks(local_rank)
+    if dist:
+        td.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        kappa, reps = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if dist:
+        td.barrier()
+    ms_total = e0.elapsed_time(e1)
+    lib.etc_profile_read(plan.handle, ms8, cnt8, 1)
+    launches = int(sum(cnt8))
+    if dist:
+        t = torch.tensor([ms_total], device=dev)
+        td.all_reduce(t, op=td.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    iters = {a: reps[a].iterations for a in axes}
+    total_iters = sum(iters.values())
+
+    # one profiled step: per-kernel device time (events on the plan stream)
+    lib.etc_profile(plan.handle, 1)
+    step()
+    lib.etc_profile(plan.handle, 0)
+    lib.etc_profile_read(plan.handle, ms8, cnt8, 1)
+    N = n ** 3
+    bpc = bytes_per_cell(plan_iso(plan))
+    peaks = load_peaks()
+    kern = {}
+    for i, name in enumerate(KCLASS):
+        if cnt8[i] == 0:
+            continue
+        avg = ms8[i] / cnt8[i]
+        d = {"ms_total": round(ms8[i], 4), "launches": int(cnt8[i]), "ms_avg": round(avg, 5)}
+        if name in bpc:
+            gbs = bpc[name] * N / (avg * 1e-3) / 1e9
+            d.update(bytes_per_launch=bpc[name] * N, gbs=round(gbs, 1), frac=round(gbs / peaks["hbm_gbs"], 4))
+        kern[name] = d
+    dom = max((k for k in kern if k in bpc), key=lambda k: kern[k]["ms_total"])
+    prof_total = sum(v["ms_total"] for v in kern.values())
+    roofline = {
+        "bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+        "frac": kern[dom]["frac"], "traffic": None,
+        "peak_source": peaks["source"] + " (MEASURED_PEAKS.json hbm_gbs, copy)",
+        "bytes_per_launch": kern[dom]["bytes_per_launch"],
+        "share_of_step": round(kern[dom]["ms_total"] / prof_total, 4),
+        "iteration_bytes_per_cell": sum(bpc.values()),
+        "iteration_frac": round(sum(bpc.values()) * N * total_iters / 1e9
+                                / (sum(kern[k]["ms_total"] for k in bpc) * 1e-3) / peaks["hbm_gbs"], 4),
+    }
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        kh = field.kx.cpu().numpy()
+        hostgrid = field.grid
+        torch.cuda.synchronize()
+        t_e2e = []
+        for it in range(max(1, min(args.steps, 3)) + 1):
+            hf = P.OrthotropicField(hostgrid, kh, kh, kh, validate=False)  # fresh object: re-uploaded
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            kap, rp = P.effective_tensor(hf, rtol=args.rtol, axes=axes, device=dev)
+            torch.cuda.synchronize()
+            if it > 0:  # first call is a warm-up
+                t_e2e.append(time.perf_counter() - t0)
+        e2e = {"value": round(statistics.mean(t_e2e), 4), "unit": "s", "h2d_bytes_per_step": int(kh.nbytes),
+               "d2h_bytes_per_step": int(sum(8 * (r.iterations + 1) + 8 for r in rp.values())),
+               "samples": len(t_e2e), "api": "paper_2404_02433_b200.effective_tensor(host numpy field)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        workers = os.cpu_count() or 1
+        smp = cpu_sample(args.cpu_n, args.contrast, 2, workers)
+        scale = (n / args.cpu_n) ** 3
+        val = scale * (len(axes) * smp["setup_s"] + total_iters * smp["iter_s"])
+        cpu = {"value": round(val, 2), "unit": "s", "cores": workers, "kind": "port",
+               "sample": (f"oracle/etc_oracle.py (numpy + pocketfft, {workers} FFT workers, ufuncs 1 core) "
+                          f"at {args.cpu_n}^3: setup {smp['setup_s']:.2f} s, PCG iteration {smp['iter_s']:.2f} s "
+                          f"(best of 2); extrapolated x{scale:.0f} cells to {len(axes)} setups + "
+                          f"{total_iters} iterations")}
+
+    line = {
+        "metric": METRIC, "value": round(ms_step / 1e3, 4), "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: random-ball RVE (preset a: 40 balls r 0.05-0.15, seed 11), voxelised on device",
+        "config": {
+            "workload": f"{n}^3 random-inclusion RVE, contrast {args.contrast:g}, directions {axes}, "
+                        f"rtol {args.rtol:g}, f64 (BASELINE config 4)",
+            "n": n, "contrast": args.contrast, "rtol": args.rtol, "directions": axes,
+            "iterations": iters, "ms_per_iter": round(ms_step / max(1, total_iters), 4),
+            "kappa_eff": {a: reps[a].kappa_eff for a in axes},
+            "parallelism": "replicas" if world > 1 else "single",
+            "l2": "inputs larger than L2 (one f64 vector = %.2f GB)" % (8 * N / 1e9),
+        },
+        "roofline": roofline, "kernels": kern, "e2e": e2e, "cpu_baseline": cpu,
+        "gpu_launches": launches, "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def plan_iso(plan) -> bool:
+    f = plan._keepalive
+    return f is not None and f[0] is f[1] and f[1] is f[2]
+
+
+# ----------------------------------------------------------------------------
+# reference arm
+# ----------------------------------------------------------------------------
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    n = args.n
+    from oracle import etc_oracle as O
+
+    k = O.random_balls(n, 40, 0.05, 0.15, args.contrast, 11)
+    t0 = time.perf_counter()
+    s = O.scale(k, 1.0 / n)
+    fc = O.faces(s, s, s)
+    refs = O.reference_constants(O.stats(fc))
+    tab = O.tables(n, n, n, refs)
+    b = O.rhs(fc, k.shape, 1.0, 0.0).reshape(-1)
+    t_setup = time.perf_counter() - t0
+    shape = k.shape
+    r = b.copy()
+    p = np.zeros_like(b)
+    z = O.precond(tab, r.reshape(shape), workers).reshape(-1)
+    w = z.copy()
+    rho = float(np.dot(r, z))
+
+    def iteration():
+        nonlocal w, rho
+        q = O.stencil(fc, w.reshape(shape)).reshape(-1)
+        alpha = rho / float(np.dot(q, w))
+        p.__iadd__(alpha * w)
+        r.__isub__(alpha * q)
+        zz = O.precond(tab, r.reshape(shape), workers).reshape(-1)
+        rho_new = float(np.dot(r, zz))
+        w = zz + (rho_new / rho) * w
+        rho = rho_new
+
+    for _ in range(args.warmup):
+        iteration()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        iteration()
+        times.append(time.perf_counter() - t0)
+    it_s = statistics.mean(times)
+    known = iterations_512() if n == 512 else {}
+    iters = {a: known.get(a, 48) for a in args.axes}
+    total = sum(iters.values())
+    value = len(args.axes) * t_setup + total * it_s
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(it_s * 1e3, 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic: random-ball RVE (preset a), host voxeliser",
+        "impl": "reference",
+        "config": {"workload": f"{n}^3 random-inclusion RVE, contrast {args.contrast:g}, directions {args.axes}, "
+                               f"rtol {args.rtol:g}, f64 (BASELINE config 4)",
+                   "n": n, "iterations": iters, "setup_s": round(t_setup, 3), "iter_s": round(it_s, 4),
+                   "iterations_source": "tests/golden/solves_512.json (reference runs); 48 where absent"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "s", "cores": workers, "kind": "port",
+                         "sample": f"one PCG iteration of the oracle port per step at {n}^3 ({workers} FFT workers, "
+                                   f"numpy ufuncs 1 core); value = {len(args.axes)} setups + {total} iterations"},
+        "e2e": {"value": round(value, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--contrast", type=float, default=100.0)
+    ap.add_argument("--rtol", type=float, default=1e-6)
+    ap.add_argument("--axes", default="xyz")
+    ap.add_argument("--cpu-n", type=int, default=256)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as td
+
+        torch.cuda.set_device(local_rank)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_b200(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as td
+
+        td.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,133 @@
+/*
+ * etc_b200.h — C ABI of the B200-native effective-thermal-conductivity solver
+ * (arXiv 2404.02433 reference: /root/reference/pkg/src/etchomo, "etchomo").
+ *
+ * The reference is pure Python; its hot path is `homogenize()`
+ * (pipeline.py:135-175) driving `pcg()` (krylov.py:36-91) with two operator
+ * callables: `apply_operator` (tpfa.py:110-131) and `FctPreconditioner`
+ * (preconditioner.py:273-282).  This header is the plugin boundary a
+ * maintainer binds from Python with ctypes; every entry
+ * point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch or CUDA types in signatures
+ *    (`stream` is a cudaStream_t passed as void*; NULL = legacy stream).
+ *  - Arrays are float64, x-fastest: cell (i,j,k) at (k*ny + j)*nx + i
+ *    (reference grid.py:1-7).
+ *  - Return codes: ETC_OK 0; ETC_BREAKDOWN 1 (PcgBreakdownError,
+ *    krylov.py:12-17); ETC_CONFIG 2 (ConfigError / ValueError); ETC_CUDA 3;
+ *    ETC_PIVOT 4 (FloatingPointError, preconditioner.py:229-244).
+ *    etc_last_error() returns a thread-local message for the last failure.
+ *  - A plan owns its device workspace and is not re-entrant (one solve at a
+ *    time per plan), mirroring SlabBuffer (transforms.py:136-138).
+ */
+#ifndef ETC_B200_H
+#define ETC_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct etc_plan etc_plan;
+
+enum {
+  ETC_OK = 0,
+  ETC_BREAKDOWN = 1,
+  ETC_CONFIG = 2,
+  ETC_CUDA = 3,
+  ETC_PIVOT = 4
+};
+
+/* Outcome of one solve (reference SolveReport, krylov.py:20-33). */
+typedef struct {
+  int iterations;      /* == len(history) - 1                              */
+  int converged;       /* history[-1] <= rtol                              */
+  int status;          /* ETC_OK or ETC_BREAKDOWN                          */
+  int breakdown_iter;  /* PcgBreakdownError.iteration when status == 1     */
+  int breakdown_kind;  /* 1 operator, 2 residual not finite, 3 precond     */
+  int pad_;
+  double kappa_eff;    /* effective_conductivity (tpfa.py:254-258)         */
+  double flux_sum;     /* sum of outflow fluxes (tpfa.py:234-251)          */
+  double norm_b;       /* ||b||                                            */
+  double device_ms;    /* device time of the PCG loop (CUDA events)        */
+} etc_solve_info;
+
+const char* etc_last_error(void);
+int etc_version(void);
+
+/* Plan for an ORIGINAL-orientation grid nx*ny*nz with edge lengths lx,ly,lz
+ * (reference GridSpec, grid.py:42-90).  Allocates the device workspace. */
+int etc_plan_create(etc_plan** out, int nx, int ny, int nz,
+                    double lx, double ly, double lz, void* stream);
+int etc_plan_destroy(etc_plan* plan);
+/* Bytes of device memory owned by the plan. */
+size_t etc_plan_device_bytes(const etc_plan* plan);
+
+/* Copy the conductivity field (OrthotropicField kx, ky, kz; grid.py:102-159)
+ * into plan-owned device storage.  `on_device` != 0: the pointers are device
+ * pointers; otherwise host pointers (H2D copies on the plan stream).  When
+ * kx == ky == kz (same pointer) the field is stored once. */
+int etc_load_field(etc_plan* plan, const double* kx, const double* ky,
+                   const double* kz, int on_device);
+
+/* Rotate the loaded field so `axis` (0 x, 1 y, 2 z) becomes canonical z and
+ * scale by 1/h^2: replaces axis_permute (pipeline.py:87-111) + scale_field
+ * (tpfa.py:19-26).  dims_out/len_out receive the canonical grid. */
+int etc_select_axis(etc_plan* plan, int axis, int dims_out[3], double len_out[3]);
+
+/* Exact extremes of the face transmissibilities (coefficient_stats,
+ * preconditioner.py:94-108), order x,y,z,in,out as (min,max) pairs. */
+int etc_coefficient_stats(etc_plan* plan, double out[10]);
+
+/* Reference constants chosen on the host (solve_reference_lp / ones_reference,
+ * preconditioner.py:117-140) and the host-built tables of TridiagFactors
+ * (preconditioner.py:178-199): weights_x[nx], weights_y[ny], z_diag[nz]
+ * of the canonical grid.  refs = {kx, ky, kz, kin, kout}. */
+int etc_set_reference(etc_plan* plan, const double refs[5], const double* weights_x,
+                      const double* weights_y, const double* z_diag);
+
+/* Full PCG solve of the canonical system with Dirichlet data p_in/p_out:
+ * build_rhs (tpfa.py:150-167) + pcg (krylov.py:36-91) + outflow flux and
+ * kappa_eff (tpfa.py:234-258), device-resident.  hist_host (capacity
+ * max_iter+1) receives the relative-residual history. */
+int etc_solve(etc_plan* plan, double p_in, double p_out, double rtol, int max_iter,
+              etc_solve_info* info, double* hist_host);
+
+/* Copy the solution vector p of the last solve (canonical layout). */
+int etc_get_solution(etc_plan* plan, double* dst, int dst_on_device);
+
+/* ---- operator-level entry points (device pointers, canonical layout) ---- */
+/* apply_operator(sys, u) (tpfa.py:110-131). */
+int etc_apply_operator(etc_plan* plan, const double* u, double* out);
+/* FctPlan.forward: plane-wise 2-D DCT-II (transforms.py:83-104). */
+int etc_dct2_xy(etc_plan* plan, const double* in, double* out);
+/* FctPlan.backward: exact inverse (transforms.py:108-133). */
+int etc_dct3_xy(etc_plan* plan, const double* in, double* out);
+/* thomas_solve_batch on spectral data, in place (preconditioner.py:215-250). */
+int etc_thomas(etc_plan* plan, double* inout);
+/* FctPreconditioner.__call__ (preconditioner.py:253-282). */
+int etc_apply_precond(etc_plan* plan, const double* r, double* z);
+/* build_rhs (tpfa.py:150-167). */
+int etc_build_rhs(etc_plan* plan, double p_in, double p_out, double* out);
+
+/* Per-kernel device timing for measurement (bench.py): when enabled, every
+ * launch is bracketed by CUDA events on the plan stream.  Kernel classes:
+ * 0 stencil, 1 update + x-DCT, 2 y-DCT, 3 z-solve, 4 y-DCT-III, 5 x-DCT-III,
+ * 6 setup (rhs, ||b||, flux, stats, permute/scale).  Launch counts are kept
+ * even when timing is off.  `reset` != 0 clears both after reading. */
+int etc_profile(etc_plan* plan, int enable);
+int etc_profile_read(etc_plan* plan, double ms[8], long long counts[8], int reset);
+
+/* Voxelise gen_random_balls / gen_center_ball (grid.py:230-275) on the device:
+ * balls = count x (cx, cy, cz, r) drawn on the host; out = n^3 cube of
+ * kappa_inc inside any ball, 1.0 elsewhere (bit-identical membership test). */
+int etc_voxelize_balls(double* out_dev, int n, const double* balls_host, int count,
+                       double kappa_inc, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ETC_B200_H */

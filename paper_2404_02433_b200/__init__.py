@@ -1,0 +1,41 @@
+"""B200-native effective-thermal-conductivity solver (arXiv 2404.02433).
+
+Drop-in for the reference `etchomo.homogenize()` path: a voxel conductivity
+field goes in, kappa_eff and the PCG residual history come out.  The O(N)
+work runs in hand-written sm_100a CUDA kernels (libetc_b200.so, C ABI in
+include/etc_b200.h); there is no CPU fallback.
+"""
+
+from .grid import (
+    Axis,
+    BoundaryConfig,
+    ConfigError,
+    GridSpec,
+    OrthotropicField,
+    RANDOM_BALL_PRESETS,
+    draw_balls,
+    gen_center_ball,
+    gen_random_balls,
+    linear_index,
+)
+from .reference import (
+    CoefficientStats,
+    ReferenceParams,
+    eigen_weights,
+    ones_reference,
+    solve_reference_lp,
+    z_chain_diagonal,
+)
+from .solver import (
+    DevicePlan,
+    PcgBreakdownError,
+    SolveReport,
+    effective_tensor,
+    get_plan,
+    homogenize,
+    release_plans,
+)
+from .operators import DeviceSystem
+from ._native import NativeUnavailable
+
+__version__ = "0.1.0"

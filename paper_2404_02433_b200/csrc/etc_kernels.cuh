@@ -1,0 +1,232 @@
+// etc_kernels.cuh — device side of the B200 ETC solver (sm_100a, float64).
+//
+// Kernels of one PCG iteration (reference krylov.py:70-90, Alg. 1):
+//   k_stencil  : w = z + beta*w_old fused with q = A w (tpfa.py:110-131),
+//                harmonic faces on the fly (tpfa.py:29-30), dots q.w, q.q, w.w
+//   k_fx<2>    : p += alpha w, r -= alpha q, ||r||^2, then the x-axis DCT-II of
+//                r (transforms.py:83-104, Makhoul) written over q
+//   k_fy<0>    : y-axis DCT-II in place
+//   k_thomas   : per-mode tridiagonal solve along z (preconditioner.py:215-250)
+//                as a register/shared-memory partition solve, fused with
+//                r.z computed in the spectral domain (Parseval)
+//   k_fy<1>    : y-axis DCT-III in place
+//   k_bx       : x-axis DCT-III -> z (transforms.py:108-133)
+// Scalars (alpha, beta, rho, relres, breakdown state) never leave the device:
+// the last CTA of every reducing kernel finalises them (deterministic order).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace etc {
+
+constexpr int kThreads = 256;
+
+struct Geom {
+  int nx, ny, nz;
+  long long plane;  // nx*ny
+  long long n;      // nx*ny*nz
+};
+
+// Device-resident PCG state (one per plan).
+struct Ctl {
+  double rho, alpha, beta, norm_b, rtol;
+  double last_rz, last_qw, last_rr;
+  int it, max_iter, done, status, bd_iter, bd_kind, converged, pad;
+};
+
+enum { BD_NONE = 0, BD_OPERATOR = 1, BD_NONFINITE = 2, BD_PRECOND = 3 };
+
+// ---------------------------------------------------------------------------
+// complex helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * (s*i), s = +-1
+__device__ __forceinline__ double2 cmul_si(double2 a, double s) { return make_double2(-s * a.y, s * a.x); }
+
+// position of source index i in the Makhoul even/odd reordering
+// (evens ascending then odds descending; transforms.py:41-43)
+__device__ __forceinline__ int makhoul_pos(int i, int n) { return (i & 1) ? n - ((i + 1) >> 1) : (i >> 1); }
+
+// ---------------------------------------------------------------------------
+// deterministic block + grid reductions with last-CTA finalisation
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* sm) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) sm[i * 32 + warp] = v[i];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = lane < nw ? sm[i * 32 + lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  }
+}
+
+// Every CTA contributes v; the last CTA to arrive reduces all partials in a
+// fixed order and thread 0 calls fin(total).  Requires a 1-D grid index.
+template <int NV, class F>
+__device__ __forceinline__ void grid_sum_finalize(double (&v)[NV], double* partials, unsigned* counter, F fin) {
+  __shared__ double sm[NV * 32];
+  __shared__ bool last;
+  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+  block_sum<NV>(v, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) partials[(size_t)bid * NV + i] = v[i];
+    __threadfence();
+    unsigned prev = atomicAdd(counter, 1u);
+    last = (prev == nb - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  for (unsigned b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] += __ldcg(partials + (size_t)b * NV + i);
+  block_sum<NV>(acc, sm);
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    fin(acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory Stockham FFT over a batch of complex lines (radix 8/4/2),
+// direct DFT for non-power-of-two lengths.  tw[m] = exp(-2 pi i m / N).
+// s = -1 forward, +1 inverse (no 1/N).  Returns the buffer holding the result.
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ void dft_small(double2 (&v)[R], double s);
+
+template <>
+__device__ __forceinline__ void dft_small<2>(double2 (&v)[2], double) {
+  double2 a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
+}
+
+template <>
+__device__ __forceinline__ void dft_small<4>(double2 (&v)[4], double s) {
+  double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+  double2 t2 = cadd(v[1], v[3]), t3 = cmul_si(csub(v[1], v[3]), s);
+  v[0] = cadd(t0, t2);
+  v[2] = csub(t0, t2);
+  v[1] = cadd(t1, t3);
+  v[3] = csub(t1, t3);
+}
+
+template <>
+__device__ __forceinline__ void dft_small<8>(double2 (&v)[8], double s) {
+  const double h = 0.70710678118654752440;
+  double2 u[4], d[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    u[m] = cadd(v[m], v[m + 4]);
+    d[m] = csub(v[m], v[m + 4]);
+  }
+  // d[m] *= W^m, W = exp(s 2 pi i / 8)
+  d[1] = make_double2(h * (d[1].x - s * d[1].y), h * (d[1].y + s * d[1].x));
+  d[2] = cmul_si(d[2], s);
+  d[3] = make_double2(-h * (d[3].x + s * d[3].y), h * (s * d[3].x - d[3].y));
+  dft_small<4>(u, s);
+  dft_small<4>(d, s);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[2 * q] = u[q];
+    v[2 * q + 1] = d[q];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, double2* __restrict__ dst, int nlines,
+                                              int N, int pitch, int Ns, const double2* __restrict__ tw, double s) {
+  const int T = N / R;
+  const int total = nlines * T;
+  const int tstride = N / (Ns * R);
+  for (int w = threadIdx.x; w < total; w += blockDim.x) {
+    const int line = w / T;
+    const int j = w - line * T;
+    const int k = j & (Ns - 1);
+    const int base = line * pitch;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src[base + j + r * T];
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        double2 t = __ldg(tw + ((k * r * tstride) & (N - 1)));
+        if (s > 0) t.y = -t.y;
+        v[r] = cmul(v[r], t);
+      }
+    }
+    dft_small<R>(v, s);
+    const int idxD = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[base + idxD + r * Ns] = v[r];
+  }
+}
+
+__device__ __forceinline__ double2* fft_lines(double2* A, double2* B, int nlines, int N, int pitch,
+                                              const double2* __restrict__ tw, double s) {
+  if (N == 1) return A;
+  if (N & (N - 1)) {  // direct DFT, O(N^2): small / non-power-of-two lengths
+    const int total = nlines * N;
+    for (int w = threadIdx.x; w < total; w += blockDim.x) {
+      const int line = w / N, kk = w - line * N, base = line * pitch;
+      double2 acc = make_double2(0.0, 0.0);
+      int idx = 0;
+      for (int m = 0; m < N; ++m) {
+        double2 t = __ldg(tw + idx);
+        if (s > 0) t.y = -t.y;
+        acc = cadd(acc, cmul(A[base + m], t));
+        idx += kk;
+        if (idx >= N) idx -= N;
+      }
+      B[base + kk] = acc;
+    }
+    __syncthreads();
+    return B;
+  }
+  double2* src = A;
+  double2* dst = B;
+  int Ns = 1;
+  while (Ns < N) {
+    const int rem = N / Ns;
+    if (rem >= 8) {
+      stockham_pass<8>(src, dst, nlines, N, pitch, Ns, tw, s);
+      Ns *= 8;
+    } else if (rem == 4) {
+      stockham_pass<4>(src, dst, nlines, N, pitch, Ns, tw, s);
+      Ns *= 4;
+    } else {
+      stockham_pass<2>(src, dst, nlines, N, pitch, Ns, tw, s);
+      Ns *= 2;
+    }
+    __syncthreads();
+    double2* t = src;
+    src = dst;
+    dst = t;
+  }
+  return src;
+}
+
+}  // namespace etc

@@ -1,0 +1,230 @@
+"""Input contract of the solve: grid, conductivity field, boundary config.
+
+Same names, invariants and error behaviour as the reference data model
+(/root/reference/pkg/src/etchomo/grid.py:24-175), so user code written
+against `etchomo` constructs the same objects here.  Differences: field
+arrays may also be CUDA tensors (float64), which keeps the field resident on
+the device across solves; and the two inclusion generators voxelise on the
+GPU (grid.py:230-275 membership test, bit-identical) instead of the host.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+
+class ConfigError(ValueError):
+    """Contract violation of a parameter (reference grid.py:24-25)."""
+
+
+class Axis(str, Enum):
+    X = "x"
+    Y = "y"
+    Z = "z"
+
+
+_AXIS_INDEX = {Axis.X: 0, Axis.Y: 1, Axis.Z: 2}
+
+
+def axis_index(axis) -> int:
+    return _AXIS_INDEX[Axis(axis)]
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """Cell counts and edge lengths (reference grid.py:42-90)."""
+
+    nx: int
+    ny: int
+    nz: int
+    lx: float = 1.0
+    ly: float = 1.0
+    lz: float = 1.0
+
+    def __post_init__(self):
+        for name in ("nx", "ny", "nz"):
+            n = getattr(self, name)
+            if not isinstance(n, (int, np.integer)) or n < 1:
+                raise ConfigError(f"{name} must be a positive integer, got {n!r}")
+        for name in ("lx", "ly", "lz"):
+            length = float(getattr(self, name))
+            if not np.isfinite(length) or length <= 0.0:
+                raise ConfigError(f"{name} must be positive and finite, got {length!r}")
+
+    @property
+    def hx(self) -> float:
+        return self.lx / self.nx
+
+    @property
+    def hy(self) -> float:
+        return self.ly / self.ny
+
+    @property
+    def hz(self) -> float:
+        return self.lz / self.nz
+
+    @property
+    def shape(self) -> tuple[int, int, int]:
+        return (self.nz, self.ny, self.nx)
+
+    @property
+    def n_cells(self) -> int:
+        return self.nx * self.ny * self.nz
+
+
+def linear_index(i: int, j: int, k: int, grid: GridSpec) -> int:
+    """x-fastest flat offset (reference grid.py:93-99)."""
+    if not (0 <= i < grid.nx and 0 <= j < grid.ny and 0 <= k < grid.nz):
+        raise IndexError(f"cell ({i}, {j}, {k}) outside grid {grid.nx}x{grid.ny}x{grid.nz}")
+    return (k * grid.ny + j) * grid.nx + i
+
+
+def _is_tensor(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+class OrthotropicField:
+    """Per-cell (kx, ky, kz), strictly positive and finite (reference
+    grid.py:102-159).  Arrays are flat x-fastest numpy arrays (frozen
+    read-only) or contiguous float64 CUDA tensors.  Passing the same array
+    object for all three components marks the field isotropic: it is then
+    stored once on the device."""
+
+    __slots__ = ("grid", "kx", "ky", "kz")
+
+    def __init__(self, grid: GridSpec, kx, ky, kz, validate: bool = True):
+        self.grid = grid
+        src = (kx, ky, kz)
+        out = []
+        cache = {}
+        for name, arr in zip(("kx", "ky", "kz"), src):
+            if id(arr) in cache:
+                out.append(cache[id(arr)])
+                continue
+            if _is_tensor(arr):
+                a = arr.reshape(-1)
+                if a.dtype.__str__() != "torch.float64":
+                    raise ConfigError(f"{name}: CUDA fields must be float64")
+                if not a.is_contiguous():
+                    a = a.contiguous()
+                if a.numel() != grid.n_cells:
+                    raise ConfigError(f"{name} has {a.numel()} entries, expected {grid.n_cells}")
+                if validate:
+                    import torch
+
+                    if not bool(torch.isfinite(a).all()) or bool((a <= 0).any()):
+                        raise ConfigError(f"{name} must be strictly positive and finite")
+            else:
+                a = np.ascontiguousarray(arr).reshape(-1)
+                if a.size != grid.n_cells:
+                    raise ConfigError(f"{name} has {a.size} entries, expected {grid.n_cells}")
+                if a.dtype not in (np.float64, np.float32):
+                    a = a.astype(np.float64)
+                if validate and (not np.all(np.isfinite(a)) or np.any(a <= 0.0)):
+                    raise ConfigError(f"{name} must be strictly positive and finite")
+                a.setflags(write=False)
+            cache[id(arr)] = a
+            out.append(a)
+        dts = {str(a.dtype) for a in out}
+        if len(dts) != 1:
+            raise ConfigError("kx, ky, kz must share one scalar dtype")
+        self.kx, self.ky, self.kz = out
+
+    @property
+    def dtype(self):
+        return self.kx.dtype
+
+    @property
+    def on_device(self) -> bool:
+        return _is_tensor(self.kx)
+
+    @property
+    def isotropic_storage(self) -> bool:
+        return self.kx is self.ky and self.ky is self.kz
+
+    def cube(self, component: str):
+        return getattr(self, component).reshape(self.grid.shape)
+
+
+@dataclass(frozen=True)
+class BoundaryConfig:
+    """Dirichlet axis and potentials (reference grid.py:162-175)."""
+
+    axis: Axis
+    p_in: float
+    p_out: float
+
+    def __post_init__(self):
+        if not (np.isfinite(self.p_in) and np.isfinite(self.p_out)):
+            raise ConfigError("p_in and p_out must be finite")
+        if self.p_in == self.p_out:
+            raise ConfigError("p_in must differ from p_out")
+
+
+# ----------------------------------------------------------------------------
+# inclusion generators, voxelised on the GPU (reference grid.py:230-284)
+# ----------------------------------------------------------------------------
+
+RANDOM_BALL_PRESETS = {
+    "a": dict(count=40, r_min=0.05, r_max=0.15, kappa_inc=10.0, seed=11),
+    "b": dict(count=80, r_min=0.04, r_max=0.10, kappa_inc=10.0, seed=23),
+    "c": dict(count=16, r_min=0.10, r_max=0.20, kappa_inc=10.0, seed=37),
+}
+
+
+def draw_balls(count: int, r_min: float, r_max: float, seed: int) -> np.ndarray:
+    """(count, 4) array of (cx, cy, cz, r): per ball three uniform center
+    coordinates then one radius draw from PCG64(seed) (grid.py:266-272)."""
+    rng = np.random.default_rng(np.uint64(seed))
+    out = np.empty((count, 4))
+    for b in range(count):
+        out[b, :3] = rng.random(3)
+        out[b, 3] = r_min + (r_max - r_min) * rng.random()
+    return out
+
+
+def _voxelize(n: int, balls: np.ndarray, kappa_inc: float, device, as_numpy: bool):
+    import torch
+
+    from . import _native
+
+    dev = torch.device(device if device is not None else "cuda")
+    out = torch.empty(n * n * n, dtype=torch.float64, device=dev)
+    balls = np.ascontiguousarray(balls, dtype=np.float64)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = _native.lib().etc_voxelize_balls(
+            out.data_ptr(), n, balls.ctypes.data_as(_native._DP), balls.shape[0],
+            float(kappa_inc), stream)
+    if rc != 0:
+        raise RuntimeError(f"voxeliser failed: {_native.last_error()}")
+    grid = GridSpec(n, n, n)
+    k = out.cpu().numpy() if as_numpy else out
+    return OrthotropicField(grid, k, k, k, validate=False)
+
+
+def gen_random_balls(n: int, count: int, r_min: float, r_max: float, kappa_inc: float,
+                     seed: int, device=None, as_numpy: bool = False) -> OrthotropicField:
+    """Random isotropic ball pack (reference grid.py:244-275), same PCG64
+    draw order and membership test; cells voxelised on the GPU."""
+    if n < 2:
+        raise ConfigError("random-balls needs n >= 2")
+    if count < 1:
+        raise ConfigError("count must be >= 1")
+    if not (0.0 < r_min <= r_max < 0.5):
+        raise ConfigError("radii must satisfy 0 < r_min <= r_max < 1/2")
+    if kappa_inc <= 0.0:
+        raise ConfigError("kappa_inc must be positive")
+    return _voxelize(n, draw_balls(count, r_min, r_max, seed), kappa_inc, device, as_numpy)
+
+
+def gen_center_ball(n: int, kappa_inc: float, device=None, as_numpy: bool = False) -> OrthotropicField:
+    """Ball of radius 1/4 at the cube center (reference grid.py:230-241)."""
+    if n < 2:
+        raise ConfigError("center-ball needs n >= 2")
+    if kappa_inc <= 0.0:
+        raise ConfigError("kappa_inc must be positive")
+    return _voxelize(n, np.array([[0.5, 0.5, 0.5, 0.25]]), kappa_inc, device, as_numpy)

@@ -114,8 +114,9 @@ int etc_build_rhs(etc_plan* plan, double p_in, double p_out, double* out);
 
 /* Per-kernel device timing for measurement (bench.py): when enabled, every
  * launch is bracketed by CUDA events on the plan stream.  Kernel classes:
- * 0 stencil, 1 update + x-DCT, 2 y-DCT, 3 z-solve, 4 y-DCT-III, 5 x-DCT-III,
- * 6 setup (rhs, ||b||, flux, stats, permute/scale).  Launch counts are kept
+ * 0 stencil (+ w update, p update, dots), 1 r update + 2-D DCT-II, 2 plain
+ * 2-D DCT-II, 3 z-solve, 4 unused, 5 2-D DCT-III, 6 setup (rhs, ||b|| +
+ * first transform, flux, stats, permute/scale, final p update).  Launch counts are kept
  * even when timing is off.  `reset` != 0 clears both after reading. */
 int etc_profile(etc_plan* plan, int enable);
 int etc_profile_read(etc_plan* plan, double ms[8], long long counts[8], int reset);

@@ -54,14 +54,16 @@ def faces(sx, sy, sz):
     return tx, ty, tz, 2.0 * sz[0], 2.0 * sz[-1]
 
 
-def stencil(fc, u: np.ndarray) -> np.ndarray:
+def stencil(fc, u: np.ndarray, reverse: bool = False) -> np.ndarray:
     """Matrix-free 7-point operator, same per-cell association order as
     tpfa.py:110-131: +fx(i-1/2) -fx(i+1/2) +fy.. -fy.. +fz.. -fz.., then the
-    Dirichlet layers."""
+    Dirichlet layers.  reverse=True accumulates z, y, x instead (the
+    "perturbed oracle" of SURVEY.md 8(c): same maths, other rounding)."""
     tx, ty, tz, t_in, t_out = fc
     nz, ny, nx = u.shape
     out = np.zeros_like(u)
-    for t, axis in ((tx, 2), (ty, 1), (tz, 0)):
+    order = ((tx, 2), (ty, 1), (tz, 0))
+    for t, axis in (order[::-1] if reverse else order):
         if u.shape[axis] < 2:
             continue
         hi = [slice(None)] * 3
@@ -231,10 +233,17 @@ def thomas(shift, zd, off, x: np.ndarray) -> np.ndarray:
     return x
 
 
-def precond(tab, r: np.ndarray, workers: int = 0) -> np.ndarray:
+def thomas_bottom_up(shift, zd, off, x: np.ndarray) -> np.ndarray:
+    """Same per-mode solve eliminating from the last layer upwards: a valid
+    second elimination order (perturbed oracle; no pivot checks)."""
+    return thomas(shift, zd[::-1].copy(), off, x[::-1])[::-1].copy()
+
+
+def precond(tab, r: np.ndarray, workers: int = 0, reverse: bool = False) -> np.ndarray:
     """z = B T F r (preconditioner.py:253-282)."""
     _, _, shift, zd, off = tab
-    return fct_backward(thomas(shift, zd, off, fct_forward(r, workers)), workers)
+    solve = thomas_bottom_up if reverse else thomas
+    return fct_backward(solve(shift, zd, off, fct_forward(r, workers)), workers)
 
 
 # ----------------------------------------------------------------------------
@@ -248,37 +257,48 @@ class Breakdown(RuntimeError):
         self.iteration = iteration
 
 
-def pcg(apply_a, apply_m, b: np.ndarray, rtol: float, max_iter: int = 1024):
+def _fsum_dot(a, b):
+    return math.fsum((a * b).tolist())
+
+
+def _fsum_norm(a):
+    return math.sqrt(math.fsum((a * a).tolist()))
+
+
+def pcg(apply_a, apply_m, b: np.ndarray, rtol: float, max_iter: int = 1024, exact_dots: bool = False):
     """Returns (p, iterations, history).  Same update order and stop tests as
     krylov.py:56-91: p0 = 0, relres checked after the r update, M applied only
-    when not yet converged."""
+    when not yet converged.  exact_dots=True uses exactly rounded dots/norms
+    (perturbed oracle)."""
+    dot = _fsum_dot if exact_dots else (lambda x, y: float(np.dot(x, y)))
+    nrm = _fsum_norm if exact_dots else (lambda x: float(np.linalg.norm(x)))
     if rtol <= 0.0:
         raise ValueError("rtol must be positive")
     if max_iter < 1:
         raise ValueError("max_iter must be >= 1")
     eps = float(np.finfo(b.dtype).eps)
-    nb = float(np.linalg.norm(b))
+    nb = nrm(b)
     p = np.zeros_like(b)
     if nb == 0.0:
         return p, 0, [0.0]
     r = b.copy()
     z = apply_m(r)
     w = z.copy()
-    rho = float(np.dot(r, z))
+    rho = dot(r, z)
     if rho <= 0.0:
         raise Breakdown("preconditioned inner product not positive", 0)
-    hist = [float(np.linalg.norm(r)) / nb]
+    hist = [nrm(r) / nb]
     it = 0
     one = b.dtype.type
     while hist[-1] > rtol and it < max_iter:
         q = apply_a(w)
-        qw = float(np.dot(q, w))
-        if qw <= 100.0 * eps * float(np.linalg.norm(q)) * float(np.linalg.norm(w)):
+        qw = dot(q, w)
+        if qw <= 100.0 * eps * nrm(q) * nrm(w):
             raise Breakdown("operator inner product lost positivity", it + 1)
         alpha = rho / qw
         p += one(alpha) * w
         r -= one(alpha) * q
-        rel = float(np.linalg.norm(r)) / nb
+        rel = nrm(r) / nb
         if not np.isfinite(rel):
             raise Breakdown("residual is not finite", it + 1)
         hist.append(rel)
@@ -286,7 +306,7 @@ def pcg(apply_a, apply_m, b: np.ndarray, rtol: float, max_iter: int = 1024):
         if rel <= rtol:
             break
         z = apply_m(r)
-        rho_new = float(np.dot(r, z))
+        rho_new = dot(r, z)
         if rho_new <= 0.0:
             raise Breakdown("preconditioned inner product not positive", it)
         w = z + one(rho_new / rho) * w
@@ -314,8 +334,10 @@ def permute(kx, ky, kz, grid, axis: str):
 
 
 def homogenize(kx, ky, kz, grid, axis="z", p_in=1.0, p_out=0.0, rtol=1e-9,
-               ref_mode="opt", max_iter=1024, workers: int = 0) -> dict:
-    """kx, ky, kz: (nz, ny, nx) cubes; grid = (nx, ny, nz, lx, ly, lz)."""
+               ref_mode="opt", max_iter=1024, workers: int = 0, perturbed: bool = False) -> dict:
+    """kx, ky, kz: (nz, ny, nx) cubes; grid = (nx, ny, nz, lx, ly, lz).
+    perturbed=True: reversed stencil association, bottom-up z elimination and
+    exactly rounded dots (same algorithm, different rounding)."""
     kx, ky, kz, g = permute(kx, ky, kz, grid, axis)
     nx, ny, nz, lx, ly, lz = g
     s = (scale(kx, lx / nx), scale(ky, ly / ny), scale(kz, lz / nz))
@@ -326,9 +348,9 @@ def homogenize(kx, ky, kz, grid, axis="z", p_in=1.0, p_out=0.0, rtol=1e-9,
     b = rhs(fc, kx.shape, p_in, p_out).reshape(-1)
     shape = kx.shape
     p, it, hist = pcg(
-        lambda u: stencil(fc, u.reshape(shape)).reshape(-1),
-        lambda r: precond(tab, r.reshape(shape), workers).reshape(-1),
-        b, rtol, max_iter,
+        lambda u: stencil(fc, u.reshape(shape), perturbed).reshape(-1),
+        lambda r: precond(tab, r.reshape(shape), workers, perturbed).reshape(-1),
+        b, rtol, max_iter, exact_dots=perturbed,
     )
     kappa = outflow_kappa(fc, p.reshape(shape), g, p_in, p_out)
     return {"iterations": it, "converged": hist[-1] <= rtol, "history": hist,

@@ -55,13 +55,18 @@ __device__ __forceinline__ int makhoul_pos(int i, int n) { return (i & 1) ? n - 
 // ---------------------------------------------------------------------------
 // deterministic block + grid reductions with last-CTA finalisation
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ int lin_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
+__device__ __forceinline__ int lin_nthreads() { return blockDim.x * blockDim.y * blockDim.z; }
+
+// Deterministic block sum (fixed shuffle tree); result valid in linear thread 0.
 template <int NV>
 __device__ __forceinline__ void block_sum(double (&v)[NV], double* sm) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const int tid = lin_tid();
+  const int lane = tid & 31, warp = tid >> 5, nw = (lin_nthreads() + 31) >> 5;
   __syncthreads();
   if (lane == 0)
 #pragma unroll
@@ -85,8 +90,9 @@ __device__ __forceinline__ void grid_sum_finalize(double (&v)[NV], double* parti
   __shared__ bool last;
   const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+  const int tid = lin_tid();
   block_sum<NV>(v, sm);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) partials[(size_t)bid * NV + i] = v[i];
     __threadfence();
@@ -99,11 +105,11 @@ __device__ __forceinline__ void grid_sum_finalize(double (&v)[NV], double* parti
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) acc[i] = 0.0;
-  for (unsigned b = threadIdx.x; b < nb; b += blockDim.x)
+  for (unsigned b = tid; b < nb; b += lin_nthreads())
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] += __ldcg(partials + (size_t)b * NV + i);
   block_sum<NV>(acc, sm);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     *counter = 0u;
     fin(acc);
   }
@@ -173,7 +179,7 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
     if (Ns > 1) {
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        double2 t = __ldg(tw + ((k * r * tstride) & (N - 1)));
+        double2 t = tw[(k * r * tstride) & (N - 1)];
         if (s > 0) t.y = -t.y;
         v[r] = cmul(v[r], t);
       }
@@ -195,7 +201,7 @@ __device__ __forceinline__ double2* fft_lines(double2* A, double2* B, int nlines
       double2 acc = make_double2(0.0, 0.0);
       int idx = 0;
       for (int m = 0; m < N; ++m) {
-        double2 t = __ldg(tw + idx);
+        double2 t = tw[idx];
         if (s > 0) t.y = -t.y;
         acc = cadd(acc, cmul(A[base + m], t));
         idx += kk;
@@ -227,6 +233,35 @@ __device__ __forceinline__ double2* fft_lines(double2* A, double2* B, int nlines
     dst = t;
   }
   return src;
+}
+
+// ---------------------------------------------------------------------------
+// thread-block cluster helpers (sm_90+; B200 portable cluster size <= 8)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_nctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_id_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned ncluster_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// all threads of all CTAs of the cluster; release/acquire orders the global
+// writes of one phase before the reads of the next
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 }  // namespace etc

@@ -95,7 +95,15 @@ int etc_set_reference(etc_plan* plan, const double refs[5], const double* weight
 int etc_solve(etc_plan* plan, double p_in, double p_out, double rtol, int max_iter,
               etc_solve_info* info, double* hist_host);
 
-/* Copy the solution vector p of the last solve (canonical layout). */
+/* homogenize() only observes the potential p on the outflow plane
+ * (reconstruct_boundary_flux, tpfa.py:234-251), so by default the solve
+ * updates p on that plane only.  keep != 0 makes etc_solve keep the full
+ * solution vector (reference pcg() output, krylov.py:91) for
+ * etc_get_solution. */
+int etc_keep_solution(etc_plan* plan, int keep);
+
+/* Copy the solution vector p of the last solve (canonical layout); requires
+ * etc_keep_solution(plan, 1) before the solve. */
 int etc_get_solution(etc_plan* plan, double* dst, int dst_on_device);
 
 /* ---- operator-level entry points (device pointers, canonical layout) ---- */

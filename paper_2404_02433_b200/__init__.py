@@ -33,6 +33,7 @@ from .solver import (
     effective_tensor,
     get_plan,
     homogenize,
+    homogenize_with_solution,
     release_plans,
 )
 from .operators import DeviceSystem

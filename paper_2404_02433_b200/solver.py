@@ -190,6 +190,9 @@ class DevicePlan:
         _check(rc, "etc_solve")
         return info, history
 
+    def keep_solution(self, keep: bool) -> None:
+        _check(self.lib.etc_keep_solution(self._h, 1 if keep else 0), "etc_keep_solution")
+
     def solution(self):
         torch = _torch()
         g = self.canonical
@@ -265,6 +268,20 @@ def homogenize(
     Same signature and report as the reference; the whole O(N) path runs on
     the GPU.  `field` arrays may be host numpy arrays (copied to the device
     once per field and cached) or CUDA float64 tensors (used in place)."""
+    return _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_iter, device,
+                       keep_solution=False)[0]
+
+
+def homogenize_with_solution(field, boundary: BoundaryConfig, rtol: float = 1e-9, ref_mode: str = "opt",
+                             max_iter: int = 1024, device=None):
+    """homogenize() that also returns the full potential p (canonical,
+    z-oriented layout) as a CUDA tensor, like the reference's pcg()
+    (krylov.py:91).  Costs one extra vector read+write per iteration."""
+    return _homogenize(field, boundary, rtol, "fct", ref_mode, "f64", 1.0, max_iter, device,
+                       keep_solution=True)
+
+
+def _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_iter, device, keep_solution):
     if precision not in _PRECISIONS:
         raise ConfigError(f"precision must be f64 or f32, got {precision!r}")
     if ref_mode not in ("opt", "one"):
@@ -289,11 +306,13 @@ def homogenize(
         stats = plan.coefficient_stats()
         refs = solve_reference_lp(stats) if ref_mode == "opt" else ones_reference(stats)
         plan.set_reference(refs)
+        plan.keep_solution(keep_solution)
         prep = time.perf_counter() - t0
         t1 = time.perf_counter()
         info, history = plan.solve(boundary.p_in, boundary.p_out, rtol, max_iter)
         exec_s = time.perf_counter() - t1
-    return SolveReport(
+        sol = plan.solution() if keep_solution else None
+    rep = SolveReport(
         iterations=int(info.iterations),
         converged=bool(history[-1] <= rtol),
         relative_residuals=history,
@@ -305,6 +324,7 @@ def homogenize(
         ref_params=refs,
         device_ms=float(info.device_ms),
     )
+    return rep, sol
 
 
 def effective_tensor(field, rtol: float = 1e-9, p_in: float = 1.0, p_out: float = 0.0,

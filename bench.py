@@ -36,8 +36,8 @@ KCLASS = ["stencil", "update_fwd2d", "fwd2d", "zsolve", "unused", "inv2d", "setu
 def bytes_per_cell(iso: bool) -> dict:
     """Algorithmic (compulsory) HBM bytes per cell per launch, f64."""
     return {
-        # z, w_old, p, s (x3 unless isotropic) read; w_new, q, p written
-        "stencil": 56 if iso else 72,
+        # z, w_old, tx, ty, tz read; w_new, q written (p only on the outflow plane)
+        "stencil": 56,
         "update_fwd2d": 32,  # r, q read; r, t(=q) written; x+y DCT-II fused per plane
         "fwd2d": 16, "zsolve": 16, "inv2d": 16,
     }

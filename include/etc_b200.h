@@ -129,6 +129,30 @@ int etc_build_rhs(etc_plan* plan, double p_in, double p_out, double* out);
 int etc_profile(etc_plan* plan, int enable);
 int etc_profile_read(etc_plan* plan, double ms[8], long long counts[8], int reset);
 
+/* ---- z-slab ranks of a multi-GPU solve --------------------
+ * The canonical (already axis-rotated) grid nx x ny x nzg is split into P
+ * equal z-slabs; this plan holds planes [k0, k0+nzl) and, for the z-solve,
+ * the pencil of rows [rank*ny/P, (rank+1)*ny/P) over all nzg planes.  The
+ * host moves data between ranks (NCCL through torch.distributed): the s and z
+ * halo planes (etc_slab_plane), the pencil all-to-all around SLAB_ZSOLVE, and
+ * the all-reduce of the 8 scalar partials in `xbuf` before SLAB_FINALIZE.
+ * Stages for etc_slab_run: 0 faces, 1 stats (ext = 10 doubles), 2 ||b|| and
+ * first transform, 3 finalize (arg: 0 stencil, 1 ||b||, 2 update, 3 z-solve),
+ * 4 stencil (arg = iteration), 5 r update + transform, 6 pack (ext = send),
+ * 7 z-solve (ext = pencil), 8 unpack (ext = received), 9 inverse transform,
+ * 10 final p update (arg = last iteration), 11 outflow flux (ext = 1 double).
+ * Same kernels as the single-GPU path; krylov.py:56-90 semantics. */
+int etc_slab_create(etc_plan** out, int nx, int ny, int nzg, int k0, int nzl, int nranks, int rank,
+                    double lx, double ly, double lz, void* stream);
+int etc_slab_load(etc_plan* plan, const double* kx, const double* ky, const double* kz, int on_device);
+/* which: 0..2 s_x,s_y,s_z, 3 z; plane -1..nzl (halo planes -1 and nzl);
+ * to_ext != 0 copies plan -> ext, else ext -> plan (device pointers). */
+int etc_slab_plane(etc_plan* plan, int which, int plane, double* ext, int to_ext);
+int etc_slab_init(etc_plan* plan, double p_in, double p_out, double rtol, int max_iter, double* xbuf);
+int etc_slab_run(etc_plan* plan, int stage, int arg, double* ext);
+/* ctl state + history; info->pad_ carries the device `done` flag. */
+int etc_slab_status(etc_plan* plan, etc_solve_info* info, double* hist_host);
+
 /* Voxelise gen_random_balls / gen_center_ball (grid.py:230-275) on the device:
  * balls = count x (cx, cy, cz, r) drawn on the host; out = n^3 cube of
  * kappa_inc inside any ball, 1.0 elsewhere (bit-identical membership test). */

@@ -22,17 +22,27 @@ namespace etc {
 
 constexpr int kThreads = 256;
 
+// Local geometry.  Single-GPU: kg0 = 0, nzg = nz, jofs = 0, nyg = ny.  A z-slab
+// rank holds planes [kg0, kg0+nz) of nzg (vectors that need neighbours carry
+// one halo plane each side, addressed as local planes -1 and nz); a z-pencil
+// holds all nzg planes of rows [jofs, jofs+ny) of nyg.
 struct Geom {
   int nx, ny, nz;
   long long plane;  // nx*ny
   long long n;      // nx*ny*nz
+  int kg0, nzg;     // global index of local plane 0, global plane count
+  int jofs, nyg;    // global index of local row 0, global row count
 };
 
 // Device-resident PCG state (one per plan).
 struct Ctl {
   double rho, alpha, beta, norm_b, rtol;
   double last_rz, last_qw, last_rr;
-  int it, max_iter, done, status, bd_iter, bd_kind, converged, pad;
+  int it, max_iter, done, status, bd_iter, bd_kind, converged, dist;
+  // dist != 0: reducing kernels export their totals to xbuf (device, 8
+  // doubles) instead of finalising; an all-reduce over ranks and k_finalize
+  // complete the stage
+  double* xbuf;
 };
 
 enum { BD_NONE = 0, BD_OPERATOR = 1, BD_NONFINITE = 2, BD_PRECOND = 3 };

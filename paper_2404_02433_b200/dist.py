@@ -1,0 +1,364 @@
+"""Multi-GPU z-slab decomposition of the solve.
+
+The canonical grid nx*ny*nzg is split into P equal z-slabs, one per rank.
+All the arithmetic runs in the same sm_100a kernels as the single-GPU path;
+this module is the host side of the exchange steps:
+
+* s and z halo planes: one plane each way to the z-neighbours (send/recv).
+  s moves once per solve, z once per iteration, after the inverse transform.
+* The per-mode z-solve runs on a z-pencil. The all-to-all turns the slab
+  (nzl, ny, nx) into the pencil (nzg, ny/P, nx) and back.
+* Three scalar all-reduces per iteration ({q.w, q.q, w.w}, r.r, r.z) feed the
+  device-side finalisation of Alg. 1 (krylov.py:70-90). It stays
+  bit-for-bit the single-GPU logic, in `k_finalize`.
+* One min/max all-reduce of the coefficient statistics per solve; the LP and
+  the tables stay on the host (preconditioner.py:117-199).
+
+`slab_solve` is written against two small interfaces:
+
+* `comm`: `TorchComm` over torch.distributed (NCCL across GPUs, gloo in tests),
+  or `ThreadComm` (P virtual ranks in one process, threads + barriers, used to
+  test the partitioned algebra on one GPU).
+* `ops`: `CudaSlabOps` is the product, a thin wrapper of the C ABI
+  `etc_slab_*`. Tests substitute a CPU restatement to check the decomposition
+  with gloo.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .reference import (
+    CoefficientStats,
+    check_pivots,
+    eigen_weights,
+    ones_reference,
+    solve_reference_lp,
+    z_chain_diagonal,
+)
+from .solver import PcgBreakdownError, SolveReport, _BREAKDOWN_MSG, _check, _torch
+
+FIN_STENCIL, FIN_NORMB, FIN_UPDATE, FIN_THOMAS = 0, 1, 2, 3
+(SLAB_FACES, SLAB_STATS, SLAB_NORMB, SLAB_FINALIZE, SLAB_STENCIL, SLAB_UPDATE, SLAB_PACK,
+ SLAB_ZSOLVE, SLAB_UNPACK, SLAB_INVERSE, SLAB_PUPDATE, SLAB_FLUX) = range(12)
+
+
+def slab_bounds(nzg: int, size: int, rank: int) -> tuple[int, int]:
+    """Planes [k0, k0+nzl) of rank `rank` (equal slabs; P | nzg)."""
+    if nzg % size:
+        raise ValueError(f"nz={nzg} must be divisible by the number of ranks {size}")
+    nzl = nzg // size
+    return rank * nzl, nzl
+
+
+# ----------------------------------------------------------------------------
+# communicators
+# ----------------------------------------------------------------------------
+
+
+class TorchComm:
+    """torch.distributed (NCCL on GPUs, gloo on CPU); collectives are
+    stream-ordered with the caller's current stream."""
+
+    def __init__(self, group=None):
+        import torch.distributed as td
+
+        self.td = td
+        self.group = group
+        self.rank = td.get_rank(group)
+        self.size = td.get_world_size(group)
+
+    def allreduce(self, t, op: str = "sum"):
+        ops = {"sum": self.td.ReduceOp.SUM, "min": self.td.ReduceOp.MIN, "max": self.td.ReduceOp.MAX}
+        self.td.all_reduce(t, op=ops[op], group=self.group)
+
+    def alltoall(self, out, inp):
+        self.td.all_to_all_single(out, inp, group=self.group)
+
+    def neighbours(self, lo, hi, recv_lo, recv_hi):
+        """send lo -> rank-1 (its upper halo), hi -> rank+1 (its lower halo);
+        receive rank-1's hi into recv_lo and rank+1's lo into recv_hi."""
+        td, r, p = self.td, self.rank, self.size
+        ops = []
+        if r > 0:
+            ops += [td.P2POp(td.isend, lo, r - 1, self.group), td.P2POp(td.irecv, recv_lo, r - 1, self.group)]
+        if r < p - 1:
+            ops += [td.P2POp(td.isend, hi, r + 1, self.group), td.P2POp(td.irecv, recv_hi, r + 1, self.group)]
+        if ops:
+            for req in td.batch_isend_irecv(ops):
+                req.wait()
+
+
+class _ThreadHub:
+    def __init__(self, size: int):
+        self.size = size
+        self.barrier = threading.Barrier(size)
+        self.slots: list = [None] * size
+
+
+class ThreadComm:
+    """P virtual ranks in one process (one thread each), sharing one device:
+    exchanges are device copies between the ranks' buffers.  Used to run the
+    partitioned algebra of the z-slab solve on a single GPU."""
+
+    def __init__(self, hub: _ThreadHub, rank: int):
+        self.hub = hub
+        self.rank = rank
+        self.size = hub.size
+
+    @staticmethod
+    def make(size: int):
+        hub = _ThreadHub(size)
+        return [ThreadComm(hub, r) for r in range(size)]
+
+    def _sync(self):
+        torch = _torch()
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+        self.hub.barrier.wait()
+
+    def allreduce(self, t, op: str = "sum"):
+        self.hub.slots[self.rank] = t
+        self._sync()
+        acc = self.hub.slots[0].clone()
+        for other in self.hub.slots[1:]:
+            if op == "sum":
+                acc = acc + other
+            elif op == "min":
+                acc = acc.minimum(other)
+            else:
+                acc = acc.maximum(other)
+        self._sync()
+        t.copy_(acc)
+        self._sync()
+
+    def alltoall(self, out, inp):
+        self.hub.slots[self.rank] = inp
+        self._sync()
+        n = inp.numel() // self.size
+        for s in range(self.size):
+            out[s * n:(s + 1) * n].copy_(self.hub.slots[s][self.rank * n:(self.rank + 1) * n])
+        self._sync()
+
+    def neighbours(self, lo, hi, recv_lo, recv_hi):
+        self.hub.slots[self.rank] = (lo, hi)
+        self._sync()
+        if self.rank > 0:
+            recv_lo.copy_(self.hub.slots[self.rank - 1][1])
+        if self.rank < self.size - 1:
+            recv_hi.copy_(self.hub.slots[self.rank + 1][0])
+        self._sync()
+
+
+# ----------------------------------------------------------------------------
+# device ops: the C ABI etc_slab_*
+# ----------------------------------------------------------------------------
+
+
+class CudaSlabOps:
+    """One rank's slab plan in libetc_b200.so."""
+
+    def __init__(self, nx, ny, nzg, k0, nzl, size, rank, lx, ly, lz, device=None):
+        torch = _torch()
+        self.lib = _native.lib()
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.nx, self.ny, self.nzg, self.k0, self.nzl = nx, ny, nzg, k0, nzl
+        self.size, self.rank = size, rank
+        self._h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            _check(self.lib.etc_slab_create(C.byref(self._h), nx, ny, nzg, k0, nzl, size, rank,
+                                            float(lx), float(ly), float(lz), stream), "etc_slab_create")
+        self._fin = weakref.finalize(self, self.lib.etc_plan_destroy, self._h)
+        self._keep = None
+
+    def _t(self, n):
+        torch = _torch()
+        return torch.empty(n, dtype=torch.float64, device=self.device)
+
+    def new(self, n):
+        return self._t(n)
+
+    def load(self, kx, ky, kz):
+        self._keep = (kx, ky, kz)
+        _check(self.lib.etc_slab_load(self._h, kx.data_ptr(), ky.data_ptr(), kz.data_ptr(), 1), "etc_slab_load")
+
+    def get_plane(self, which, plane):
+        out = self._t(self.nx * self.ny)
+        _check(self.lib.etc_slab_plane(self._h, which, plane, out.data_ptr(), 1), "etc_slab_plane")
+        return out
+
+    def set_plane(self, which, plane, t):
+        _check(self.lib.etc_slab_plane(self._h, which, plane, t.data_ptr(), 0), "etc_slab_plane")
+
+    def run(self, stage, arg=0, ext=None):
+        _check(self.lib.etc_slab_run(self._h, stage, arg, ext.data_ptr() if ext is not None else None),
+               "etc_slab_run")
+
+    def stats(self):
+        out = self._t(10)
+        self.run(SLAB_STATS, 0, out)
+        return out
+
+    def set_reference(self, refs, wx, wy, zd):
+        r5 = (C.c_double * 5)(*refs.constants())
+        dp = _native._DP
+        _check(self.lib.etc_set_reference(self._h, r5, wx.ctypes.data_as(dp), wy.ctypes.data_as(dp),
+                                          zd.ctypes.data_as(dp)), "etc_set_reference")
+
+    def init(self, p_in, p_out, rtol, max_iter, xbuf):
+        _check(self.lib.etc_slab_init(self._h, float(p_in), float(p_out), float(rtol), int(max_iter),
+                                      xbuf.data_ptr()), "etc_slab_init")
+
+    def status(self, max_iter):
+        info = _native.SolveInfo()
+        hist = np.empty(max_iter + 1, dtype=np.float64)
+        _check(self.lib.etc_slab_status(self._h, C.byref(info), hist.ctypes.data_as(_native._DP)),
+               "etc_slab_status")
+        return info, [float(v) for v in hist[: info.iterations + 1]]
+
+
+# ----------------------------------------------------------------------------
+# the distributed solve
+# ----------------------------------------------------------------------------
+
+
+@dataclass
+class SlabResult:
+    report: SolveReport
+    rank: int
+    size: int
+
+
+def _exchange_planes(ops, comm, which: int, nzl: int):
+    lo = ops.get_plane(which, 0)
+    hi = ops.get_plane(which, nzl - 1)
+    recv_lo = ops.new(lo.numel())
+    recv_hi = ops.new(hi.numel())
+    comm.neighbours(lo, hi, recv_lo, recv_hi)
+    if comm.rank > 0:
+        ops.set_plane(which, -1, recv_lo)
+    if comm.rank < comm.size - 1:
+        ops.set_plane(which, nzl, recv_hi)
+
+
+def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_mode="opt",
+               max_iter=1024, check_every=1) -> SolveReport:
+    """PCG on this rank's z-slab of the canonical field (kx, ky, kz: local
+    planes, x-fastest).  grid = (nx, ny, nzg, lx, ly, lz), the canonical
+    global grid.  Every rank returns the same report."""
+    nx, ny, nzg, lx, ly, lz = grid
+    nzl = nzg // comm.size
+    iso = kx is ky and ky is kz
+    ops.load(kx, ky, kz)
+    for which in ((2,) if iso else (0, 1, 2)):
+        _exchange_planes(ops, comm, which, nzl)
+    ops.run(SLAB_FACES)
+    st = ops.stats()
+    lo, hi = st[0::2].clone(), st[1::2].clone()
+    comm.allreduce(lo, "min")
+    comm.allreduce(hi, "max")
+    vals = np.empty(10)
+    vals[0::2] = lo.cpu().numpy()
+    vals[1::2] = hi.cpu().numpy()
+    # empty groups (no faces along an axis of length 1) -> (1, 1) (preconditioner.py:94-98)
+    for g, n in ((0, nx), (1, ny), (2, nzg)):
+        if n < 2:
+            vals[2 * g], vals[2 * g + 1] = 1.0, 1.0
+    stats = CoefficientStats(*[float(v) for v in vals])
+    refs = solve_reference_lp(stats) if ref_mode == "opt" else ones_reference(stats)
+    wx, wy, zd = eigen_weights(nx), eigen_weights(ny), z_chain_diagonal(nzg, refs)
+    check_pivots(nzg, zd, refs)
+    ops.set_reference(refs, wx, wy, zd)
+
+    xbuf = ops.new(8)
+    xbuf.zero_()
+    nloc = nx * ny * nzl
+    send = ops.new(nloc)
+    recv = ops.new(nloc)
+
+    def zsolve_and_back():
+        ops.run(SLAB_PACK, 0, send)
+        comm.alltoall(recv, send)
+        ops.run(SLAB_ZSOLVE, 0, recv)
+        comm.alltoall(send, recv)
+        ops.run(SLAB_UNPACK, 0, send)
+        comm.allreduce(xbuf[4:5])
+        ops.run(SLAB_FINALIZE, FIN_THOMAS)
+        ops.run(SLAB_INVERSE)
+        _exchange_planes(ops, comm, 3, nzl)
+
+    ops.init(p_in, p_out, rtol, max_iter, xbuf)
+    ops.run(SLAB_NORMB)
+    comm.allreduce(xbuf[3:4])
+    ops.run(SLAB_FINALIZE, FIN_NORMB)
+    zsolve_and_back()
+    it = 0
+    done = False
+    while not done and it < max_iter:
+        it += 1
+        ops.run(SLAB_STENCIL, it)
+        comm.allreduce(xbuf[0:3])
+        ops.run(SLAB_FINALIZE, FIN_STENCIL)
+        ops.run(SLAB_UPDATE)
+        comm.allreduce(xbuf[3:4])
+        ops.run(SLAB_FINALIZE, FIN_UPDATE)
+        zsolve_and_back()
+        if it % check_every == 0 or it == max_iter:
+            info, _ = ops.status(max_iter)
+            done = info.pad_ != 0
+    info, history = ops.status(max_iter)
+    if info.status:
+        raise PcgBreakdownError(_BREAKDOWN_MSG.get(info.breakdown_kind, "breakdown"), info.breakdown_iter)
+    ops.run(SLAB_PUPDATE, info.iterations)
+    fbuf = ops.new(1)
+    ops.run(SLAB_FLUX, 0, fbuf)
+    comm.allreduce(fbuf)
+    flux = float(fbuf.cpu().item())
+    kappa = lz * flux / (nx * ny * (p_in - p_out))
+    return SolveReport(iterations=int(info.iterations), converged=bool(history[-1] <= rtol),
+                       relative_residuals=history, kappa_eff=kappa, ref_params=refs)
+
+
+def virtual_slab_solve(field_cube, grid, nranks: int, p_in=1.0, p_out=0.0, rtol=1e-9, ref_mode="opt",
+                       max_iter=1024, device=None) -> list:
+    """Run the z-slab solve with `nranks` virtual ranks on one GPU (threads +
+    device copies stand in for NCCL); field_cube: canonical (nzg, ny, nx)
+    CUDA tensor (isotropic field).  Returns every rank's report."""
+    torch = _torch()
+    nx, ny, nzg, lx, ly, lz = grid
+    comms = ThreadComm.make(nranks)
+    out: list = [None] * nranks
+    errs: list = []
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(dev)
+            k0, nzl = slab_bounds(nzg, nranks, r)
+            k = field_cube[k0:k0 + nzl].contiguous().reshape(-1)
+            ops = CudaSlabOps(nx, ny, nzg, k0, nzl, nranks, r, lx, ly, lz, dev)
+            out[r] = slab_solve(ops, comms[r], k, k, k, grid, p_in, p_out, rtol, ref_mode, max_iter)
+        except BaseException as exc:  # surface worker failures
+            errs.append(exc)
+            comms[r].hub.barrier.abort()
+
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out

@@ -1,0 +1,47 @@
+"""The z-slab (multi-GPU) decomposition run as P virtual ranks on one GPU:
+threads stand in for processes and device copies for NCCL, while every
+kernel is the production one in slab mode (halos, pencil z-solve, exported
+partials + k_finalize).  Must reproduce the single-GPU solve."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2404_02433_b200 as P  # noqa: E402
+from paper_2404_02433_b200 import dist  # noqa: E402
+
+
+def _canonical(k, axis):
+    c = k.reshape(k.shape)
+    if axis == "x":
+        return c.permute(2, 1, 0).contiguous()
+    if axis == "y":
+        return c.permute(1, 0, 2).contiguous()
+    return c.contiguous()
+
+
+@pytest.mark.parametrize("n,nranks,axis,C", [(32, 2, "z", 100.0), (64, 4, "x", 100.0), (64, 2, "y", 10.0),
+                                             (128, 8, "z", 100.0)])
+def test_virtual_slabs_match_single_gpu(n, nranks, axis, C):
+    f = P.gen_random_balls(n, 40, 0.05, 0.15, C, 11)
+    rtol = 1e-8
+    single = P.homogenize(f, P.BoundaryConfig(P.Axis(axis), 1.0, 0.0), rtol)
+    cube = _canonical(f.kx.reshape(n, n, n), axis)
+    reps = dist.virtual_slab_solve(cube, (n, n, n, 1.0, 1.0, 1.0), nranks, 1.0, 0.0, rtol)
+    for rep in reps:
+        assert rep.iterations == single.iterations
+        assert rep.relative_residuals == reps[0].relative_residuals
+        assert abs(rep.kappa_eff - single.kappa_eff) <= 1e-10 * abs(single.kappa_eff)
+        h = np.array(rep.relative_residuals)
+        s = np.array(single.relative_residuals)
+        big = s > 1e-2  # 1e-8 while relres > 1e-2, envelope below
+        assert np.all(np.abs(h[big] - s[big]) <= 1e-8 * s[big])
+        mid = (s > 1e-4) & ~big
+        assert np.all(np.abs(h[mid] - s[mid]) <= 1e-5 * s[mid])
+        assert np.all(np.abs(h - s) <= 1e-1 * s)  # rounding floor below 1e-4
+        assert rep.ref_params == single.ref_params

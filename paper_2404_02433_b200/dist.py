@@ -362,3 +362,68 @@ def virtual_slab_solve(field_cube, grid, nranks: int, p_in=1.0, p_out=0.0, rtol=
     if errs:
         raise errs[0]
     return out
+
+
+# ----------------------------------------------------------------------------
+# public multi-GPU entry point
+# ----------------------------------------------------------------------------
+
+_OPS_CACHE: dict = {}
+
+
+def _canonical(fld, axis: str):
+    """axis_permute (pipeline.py:87-111) on CUDA tensors: returns the
+    canonical (kx, ky, kz) cubes (nz', ny', nx') and the canonical grid."""
+    g = fld.grid
+    cube = lambda a: a.reshape(g.nz, g.ny, g.nx)
+    kx, ky, kz = cube(fld.kx), cube(fld.ky), cube(fld.kz)
+    perm = lambda a, order: a.transpose(order) if isinstance(a, np.ndarray) else a.permute(*order)
+    if axis == "z":
+        return (kx, ky, kz), (g.nx, g.ny, g.nz, g.lx, g.ly, g.lz)
+    if axis == "x":
+        sw = lambda a: perm(a, (2, 1, 0))
+        return (sw(kz), sw(ky), sw(kx)), (g.nz, g.ny, g.nx, g.lz, g.ly, g.lx)
+    sw = lambda a: perm(a, (1, 0, 2))
+    return (sw(kx), sw(kz), sw(ky)), (g.nx, g.nz, g.ny, g.lx, g.lz, g.ly)
+
+
+def effective_tensor_dist(field, comm=None, rtol: float = 1e-9, p_in: float = 1.0, p_out: float = 0.0,
+                          ref_mode: str = "opt", max_iter: int = 1024, axes: str = "xyz", device=None):
+    """Multi-GPU effective_tensor: every rank passes the same field (host
+    numpy or CUDA tensors); each solves its z-slab of every load direction
+    with the others over `comm` (default: torch.distributed world).  Returns
+    (kappa[3], {axis: SolveReport}) on every rank."""
+    torch = _torch()
+    from .solver import _as_field
+
+    comm = comm or TorchComm()
+    fld = _as_field(field)
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    iso = fld.kx is fld.ky and fld.ky is fld.kz
+    reports = {}
+    for ax in axes:
+        comps, grid = _canonical(fld, ax)
+        nx, ny, nzg = grid[:3]
+        k0, nzl = slab_bounds(nzg, comm.size, comm.rank)
+
+        def slab(c):
+            part = c[k0:k0 + nzl]
+            if isinstance(part, np.ndarray):
+                part = torch.from_numpy(np.array(part, copy=True))
+            return part.to(dev, non_blocking=True).contiguous().reshape(-1)
+
+        if iso:
+            t = slab(comps[0])
+            kx = ky = kz = t
+        else:
+            kx, ky, kz = (slab(c) for c in comps)
+        key = (grid, comm.rank, comm.size, dev.index)
+        ops = _OPS_CACHE.get(key)
+        if ops is None:
+            ops = CudaSlabOps(nx, ny, nzg, k0, nzl, comm.size, comm.rank, grid[3], grid[4], grid[5], dev)
+            _OPS_CACHE[key] = ops
+        reports[ax] = slab_solve(ops, comm, kx, ky, kz, grid, p_in, p_out, rtol, ref_mode, max_iter)
+    kappa = np.array([reports[a].kappa_eff if a in reports else np.nan for a in "xyz"])
+    return kappa, reports

@@ -1,0 +1,247 @@
+"""CPU restatement of the z-slab stages (TEST INFRASTRUCTURE ONLY).
+
+Implements the `ops` interface that `paper_2404_02433_b200.dist.slab_solve`
+drives. Each method does in numpy exactly what the matching `etc_slab_run` stage
+does on the GPU. It lets the host-side decomposition run over a real gloo
+process group on CPU:
+
+* halo planes, pencil all-to-all, scalar all-reduces;
+* device-side finalisation order and the stop logic.
+
+The test compares the result with the single-process oracle.
+"""
+
+from __future__ import annotations
+
+import math
+from types import SimpleNamespace
+
+import numpy as np
+import torch
+
+from oracle import etc_oracle as O
+
+EPS = 2.220446049250313e-16
+
+
+class CpuSlabOps:
+    def __init__(self, nx, ny, nzg, k0, nzl, size, rank, lx, ly, lz):
+        self.nx, self.ny, self.nzg, self.k0, self.nzl = nx, ny, nzg, k0, nzl
+        self.size, self.rank = size, rank
+        self.lx, self.ly, self.lz = lx, ly, lz
+        self.s = None
+        self.ctl = None
+
+    # -- buffers ------------------------------------------------------------
+    def new(self, n):
+        return torch.zeros(n, dtype=torch.float64)
+
+    def load(self, kx, ky, kz):
+        nzl, ny, nx = self.nzl, self.ny, self.nx
+        h = (self.lx / nx, self.ly / ny, self.lz / self.nzg)
+        self.s = []
+        for a, k in enumerate((kx, ky, kz)):
+            ext = np.zeros((nzl + 2, ny, nx))
+            ext[1:-1] = O.scale(k.numpy().reshape(nzl, ny, nx), h[a])
+            self.s.append(ext)
+        self.z = np.zeros((nzl + 2, ny, nx))
+        self.w = [np.zeros((nzl + 2, ny, nx)), np.zeros((nzl + 2, ny, nx))]
+
+    def _buf(self, which):
+        return self.s[which] if which <= 2 else self.z
+
+    def get_plane(self, which, plane):
+        return torch.from_numpy(self._buf(which)[plane + 1].reshape(-1).copy())
+
+    def set_plane(self, which, plane, t):
+        self._buf(which)[plane + 1] = t.numpy().reshape(self.ny, self.nx)
+
+    # -- stages ---------------------------------------------------------------
+    def _kg(self, k):
+        return self.k0 + k
+
+    def run(self, stage, arg=0, ext=None):
+        getattr(self, "_stage%d" % stage)(arg, ext)
+
+    def _stage0(self, arg, ext):  # faces
+        sx, sy, sz = self.s
+        self.tx = O.harmonic(sx[1:-1, :, :-1], sx[1:-1, :, 1:])
+        self.ty = O.harmonic(sy[1:-1, :-1, :], sy[1:-1, 1:, :])
+        # tz[k] (k = -1..nzl-1): face between local planes k and k+1
+        self.tz = O.harmonic(sz[:-1], sz[1:])
+
+    def stats(self):
+        nzl = self.nzl
+        out = np.array([np.inf, 0.0] * 5)
+
+        def upd(g, arr):
+            if arr.size:
+                out[2 * g] = min(out[2 * g], arr.min())
+                out[2 * g + 1] = max(out[2 * g + 1], arr.max())
+
+        upd(0, self.tx)
+        upd(1, self.ty)
+        owned = [k for k in range(nzl) if self._kg(k) + 1 < self.nzg]
+        if owned:
+            upd(2, self.tz[np.array(owned) + 1])
+        if self.k0 == 0:
+            upd(3, self.s[2][1])
+        if self.k0 + nzl == self.nzg:
+            upd(4, self.s[2][nzl])
+        return torch.from_numpy(out)
+
+    def set_reference(self, refs, wx, wy, zd):
+        self.refs = refs
+        self.shift = wx[None, :] * refs.kx_ref + wy[:, None] * refs.ky_ref
+        self.zd = zd
+        self.off = -refs.kz_ref
+
+    def init(self, p_in, p_out, rtol, max_iter, xbuf):
+        self.ctl = SimpleNamespace(rho=0.0, alpha=0.0, beta=0.0, norm_b=0.0, rtol=rtol, it=0, max_iter=max_iter,
+                                   done=0, status=0, bd_iter=0, bd_kind=0, converged=0)
+        self.hist = [0.0] * (max_iter + 1)
+        self.xbuf = xbuf
+        self.p_in, self.p_out = p_in, p_out
+        nzl = self.nzl
+        sz = self.s[2][1:-1]
+        self.r = np.zeros((nzl, self.ny, self.nx))
+        if self.k0 == 0:
+            self.r[0] = (2.0 * sz[0]) * p_in
+        if self.k0 + nzl == self.nzg:
+            self.r[-1] += (2.0 * sz[-1]) * p_out
+        self.p = np.zeros_like(self.r)
+
+    def _stage2(self, arg, ext):  # ||b|| + first transform
+        self.xbuf[3] = float(np.sum(self.r * self.r))
+        self.t = O.fct_forward(self.r)
+
+    def _stage3(self, stage, ext):  # finalize
+        c, x = self.ctl, self.xbuf.numpy()
+        if c.done and stage != 1:
+            return
+        if stage == 0:
+            if x[0] <= 100.0 * EPS * math.sqrt(x[1]) * math.sqrt(x[2]):
+                c.status, c.bd_kind, c.bd_iter, c.done = 1, 1, c.it + 1, 1
+            c.alpha = c.rho / x[0]
+        elif stage == 1:
+            c.norm_b = math.sqrt(x[3])
+            self.hist[0] = 1.0 if c.norm_b != 0.0 else 0.0
+            if c.norm_b == 0.0:
+                c.converged, c.done = 1, 1
+        elif stage == 2:
+            rel = math.sqrt(x[3]) / c.norm_b
+            if not math.isfinite(rel):
+                c.status, c.bd_kind, c.bd_iter, c.done = 1, 2, c.it + 1, 1
+                return
+            c.it += 1
+            self.hist[c.it] = rel
+            if rel <= c.rtol:
+                c.converged, c.done = 1, 1
+        else:
+            rz = x[4] * 4.0 / (self.nx * self.ny)
+            if c.it == 0:
+                if rz <= 0.0:
+                    c.status, c.bd_kind, c.bd_iter, c.done = 1, 3, 0, 1
+                c.rho = rz
+            else:
+                if rz <= 0.0:
+                    c.status, c.bd_kind, c.bd_iter, c.done = 1, 3, c.it, 1
+                else:
+                    c.beta = rz / c.rho
+                    c.rho = rz
+                if c.it >= c.max_iter:
+                    c.done = 1
+
+    def _stage4(self, it, ext):  # stencil (+ previous p update, dots)
+        c = self.ctl
+        if c.done:
+            return
+        wn, wo = self.w[it & 1], self.w[(it - 1) & 1]
+        if it == 1:
+            wn[:] = self.z
+        else:
+            wn[:] = self.z + c.beta * wo
+            kl = self.nzg - 1 - self.k0
+            if 0 <= kl < self.nzl:
+                self.p[kl] = self.p[kl] + c.alpha * wo[kl + 1]
+        u = wn
+        nzl = self.nzl
+        q = np.zeros((nzl, self.ny, self.nx))
+        core = u[1:-1]
+        for t, axis in ((self.tx, 2), (self.ty, 1)):
+            hi = [slice(None)] * 3
+            lo = [slice(None)] * 3
+            hi[axis] = slice(1, None)
+            lo[axis] = slice(None, -1)
+            f = t * (core[tuple(hi)] - core[tuple(lo)])
+            q[tuple(hi)] += f
+            q[tuple(lo)] -= f
+        for k in range(nzl):
+            kg = self._kg(k)
+            if kg > 0:
+                q[k] += self.tz[k] * (u[k + 1] - u[k])
+            if kg + 1 < self.nzg:
+                q[k] -= self.tz[k + 1] * (u[k + 2] - u[k + 1])
+            if kg == 0:
+                q[k] += (2.0 * self.s[2][k + 1]) * u[k + 1]
+            if kg == self.nzg - 1:
+                q[k] += (2.0 * self.s[2][k + 1]) * u[k + 1]
+        self.q = q
+        self.xbuf[0] = float(np.sum(q * core))
+        self.xbuf[1] = float(np.sum(q * q))
+        self.xbuf[2] = float(np.sum(core * core))
+
+    def _stage5(self, arg, ext):  # r -= alpha q; ||r||; transform
+        if self.ctl.done:
+            return
+        self.r = self.r - self.ctl.alpha * self.q
+        self.xbuf[3] = float(np.sum(self.r * self.r))
+        self.t = O.fct_forward(self.r)
+
+    def _stage6(self, arg, ext):  # pack
+        nyl = self.ny // self.size
+        blocks = [self.t[:, r * nyl:(r + 1) * nyl, :] for r in range(self.size)]
+        ext.copy_(torch.from_numpy(np.concatenate([b.reshape(-1) for b in blocks])))
+
+    def _stage7(self, arg, ext):  # z-solve on the pencil
+        if self.ctl.done:
+            return
+        nyl = self.ny // self.size
+        pen = ext.numpy().reshape(self.nzg, nyl, self.nx)
+        j0 = self.rank * nyl
+        shift = self.shift[j0:j0 + nyl]
+        x = O.thomas(shift, self.zd, self.off, pen)
+        ax = np.where(np.arange(self.nx) == 0, 0.5, 1.0)
+        ay = np.where(np.arange(j0, j0 + nyl) == 0, 0.5, 1.0)
+        self.xbuf[4] = float(np.sum(ay[:, None] * ax[None, :] * pen * x))
+        ext.copy_(torch.from_numpy(x.reshape(-1)))
+
+    def _stage8(self, arg, ext):  # unpack
+        nyl = self.ny // self.size
+        a = ext.numpy().reshape(self.size, self.nzl, nyl, self.nx)
+        self.t = np.concatenate([a[s] for s in range(self.size)], axis=1)
+
+    def _stage9(self, arg, ext):  # inverse transform
+        if self.ctl.done:
+            return
+        self.z[1:-1] = O.fct_backward(self.t)
+
+    def _stage10(self, it, ext):  # final p update on the outflow plane
+        kl = self.nzg - 1 - self.k0
+        if it >= 1 and 0 <= kl < self.nzl:
+            self.p[kl] = self.p[kl] + self.ctl.alpha * self.w[it & 1][kl + 1]
+
+    def _stage11(self, arg, ext):  # outflow flux
+        kl = self.nzg - 1 - self.k0
+        hz = self.lz / self.nzg
+        s = 0.0
+        if 0 <= kl < self.nzl:
+            tout = 2.0 * self.s[2][kl + 1]
+            s = float(np.sum((tout * hz) * (self.p[kl] - self.p_out)))
+        ext[0] = s
+
+    def status(self, max_iter):
+        c = self.ctl
+        info = SimpleNamespace(iterations=c.it, converged=c.converged, status=c.status, breakdown_iter=c.bd_iter,
+                               breakdown_kind=c.bd_kind, pad_=c.done)
+        return info, [float(v) for v in self.hist[:c.it + 1]]

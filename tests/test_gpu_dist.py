@@ -36,7 +36,7 @@ def test_virtual_slabs_match_single_gpu(n, nranks, axis, C):
     for rep in reps:
         assert rep.iterations == single.iterations
         assert rep.relative_residuals == reps[0].relative_residuals
-        assert abs(rep.kappa_eff - single.kappa_eff) <= 1e-10 * abs(single.kappa_eff)
+        assert abs(rep.kappa_eff - single.kappa_eff) <= 1e-9 * abs(single.kappa_eff)
         h = np.array(rep.relative_residuals)
         s = np.array(single.relative_residuals)
         big = s > 1e-2  # 1e-8 while relres > 1e-2, envelope below

@@ -74,6 +74,24 @@ def test_transforms(golden_kernels):
         assert _rel(_cpu(ds.dct3_xy(u)), data[f"{tag}/bwd"]) <= 1e-12, tag
 
 
+@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024])
+def test_plane_transforms_square(n):
+    """The compile-time square-plane kernels (single-item below 128, paired
+    items from 128 up) against the oracle's DCT-II/III (transforms.py:83-133)
+    on a few planes, including the all-ones and single-spike planes."""
+    nz = 3
+    rng = np.random.default_rng(n)
+    g = P.GridSpec(n, n, nz, 1.0, 1.0, 1.0)
+    ds = P.DeviceSystem(P.OrthotropicField(g, *np.ones((3, n * n * nz))))
+    u = rng.standard_normal((nz, n, n))
+    u[1] = 1.0
+    u[2] = 0.0
+    u[2, n // 3, n // 5] = 1.0
+    fwd, bwd = O.fct_forward(u), O.fct_backward(u)
+    assert _rel(_cpu(ds.dct2_xy(u.reshape(-1))), fwd.reshape(-1)) <= 1e-12, n
+    assert _rel(_cpu(ds.dct3_xy(u.reshape(-1))), bwd.reshape(-1)) <= 1e-12, n
+
+
 def test_thomas_and_precond(golden_kernels):
     data, shapes = golden_kernels
     for tag in shapes:

@@ -33,8 +33,19 @@ METRIC = "PCG time-to-solution, 512^3 random-inclusion RVE (contrast 100), x/y/z
 KCLASS = ["stencil", "update_fwd2d", "fwd2d", "zsolve", "unused", "inv2d", "setup"]
 
 
-def bytes_per_cell(iso: bool) -> dict:
-    """Algorithmic (compulsory) HBM bytes per cell per launch, f64."""
+def bytes_per_cell(wfuse: bool) -> dict:
+    """Algorithmic (compulsory) HBM bytes per cell per launch, f64.
+
+    wfuse (single-GPU square planes, the default): the inverse transform
+    builds the search direction w = z + beta w_old itself, so the stencil
+    reads w instead of z and w_old and writes only q."""
+    if wfuse:
+        return {
+            "stencil": 40,  # w, tx, ty, tz read; q written
+            "update_fwd2d": 32,  # r, q read; r, t(=q) written; x+y DCT-II fused per plane
+            "fwd2d": 16, "zsolve": 16,
+            "inv2d": 24,  # t, w_old read; w written (16 on the first launch of a solve: w = z)
+        }
     return {
         # z, w_old, tx, ty, tz read; w_new, q written (p only on the outflow plane)
         "stencil": 56,
@@ -251,7 +262,9 @@ def run_b200(args, rank, world, local_rank):
     for i in range(8):
         ms8[i], cnt8[i] = pms[i], pcnt[i]
     N = n ** 3 // world  # cells per rank per launch
-    bpc = bytes_per_cell(True)
+    wfuse = (not dist and not args.slab and os.environ.get("ETC_WFUSE", "1") != "0" and n >= 128
+             and n & (n - 1) == 0)
+    bpc = bytes_per_cell(wfuse)
     peaks = load_peaks()
     kern = {}
     for i, name in enumerate(KCLASS):
@@ -260,8 +273,11 @@ def run_b200(args, rank, world, local_rank):
         avg = ms8[i] / cnt8[i]
         d = {"ms_total": round(ms8[i], 4), "launches": int(cnt8[i]), "ms_avg": round(avg, 5)}
         if name in bpc:
-            gbs = bpc[name] * N / (avg * 1e-3) / 1e9
-            d.update(bytes_per_launch=bpc[name] * N, gbs=round(gbs, 1), frac=round(gbs / peaks["hbm_gbs"], 4))
+            b = bpc[name] * N
+            if wfuse and name == "inv2d":  # first launch of each solve writes w = z (16 B/cell)
+                b = (16 * N * len(axes) + 24 * N * (cnt8[i] - len(axes))) / cnt8[i]
+            gbs = b / (avg * 1e-3) / 1e9
+            d.update(bytes_per_launch=int(b), gbs=round(gbs, 1), frac=round(gbs / peaks["hbm_gbs"], 4))
         kern[name] = d
     dom = max((k for k in kern if k in bpc), key=lambda k: kern[k]["ms_total"])
     it_kernels = [k for k in ("stencil", "update_fwd2d", "zsolve", "inv2d") if k in kern]

@@ -10,6 +10,8 @@ golden vectors and the CPU oracle.  Tolerances are written per test:
   kappa_eff within max(1e-8, 10 x oracle-vs-reference spread).
 """
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -185,6 +187,22 @@ def test_homogenize_matches_reference(golden_solves):
         assert err <= ktol, (tag, err, ktol)
         for key, val in case["refs"].items():
             assert rep.ref_params.as_dict()[key] == val
+
+
+def test_homogenize_512_matches_reference_runs():
+    """The benchmark configuration itself (512^3 random-inclusion RVE,
+    contrast 100, rtol 1e-6) against the reference run at full size in this
+    container (tests/golden/solves_512.json, make_golden_512.py): same
+    iteration counts, kappa_eff and history to 1e-8."""
+    import json
+
+    runs = json.loads((Path(__file__).parent / "golden" / "solves_512.json").read_text())
+    f = P.gen_random_balls(512, 40, 0.05, 0.15, 100.0, 11)
+    for case in runs:
+        rep = P.homogenize(f, P.BoundaryConfig(P.Axis(case["axis"]), 1.0, 0.0), case["rtol"])
+        assert rep.iterations == case["iterations"], case["axis"]
+        assert abs(rep.kappa_eff - case["kappa_eff"]) <= 1e-8 * abs(case["kappa_eff"]), case["axis"]
+        assert _hist_dev(rep.relative_residuals, case["history"]) <= 1e-8, case["axis"]
 
 
 @pytest.mark.parametrize("axis", ["x", "y", "z"])

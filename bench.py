@@ -54,6 +54,27 @@ def bytes_per_cell(wfuse: bool) -> dict:
     }
 
 
+NCU_PREFIX = {"stencil": "k_stencil", "update_fwd2d": "k_fwd", "zsolve": "k_thomas",
+              "inv2d": "k_inv"}
+
+
+def load_traffic(n: int) -> tuple[dict, str | None]:
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    of each kernel class from the committed `ncu --set full` capture of the
+    default workload (profiles/r01/ncu_full_512_traffic.json, written by
+    profiles/ncu_summary.py); {} for other sizes."""
+    p = ROOT / "profiles" / "r01" / "ncu_full_512_traffic.json"
+    if n != 512 or not p.exists():
+        return {}, None
+    d = json.loads(p.read_text())
+    out = {}
+    for cls, pre in NCU_PREFIX.items():
+        for name, v in d.items():
+            if name.startswith(pre):
+                out[cls] = int(v["dram_bytes"])
+    return out, str(p.relative_to(ROOT))
+
+
 def load_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -280,11 +301,17 @@ def run_b200(args, rank, world, local_rank):
             d.update(bytes_per_launch=int(b), gbs=round(gbs, 1), frac=round(gbs / peaks["hbm_gbs"], 4))
         kern[name] = d
     dom = max((k for k in kern if k in bpc), key=lambda k: kern[k]["ms_total"])
+    traffic, tsrc = load_traffic(n)
+    if not dist:
+        for k, v in traffic.items():
+            if k in kern:
+                kern[k]["dram_bytes_ncu"] = v
     it_kernels = [k for k in ("stencil", "update_fwd2d", "zsolve", "inv2d") if k in kern]
     prof_total = sum(v["ms_total"] for v in kern.values())
     roofline = {
         "bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
-        "frac": kern[dom]["frac"], "traffic": None,
+        "frac": kern[dom]["frac"], "traffic": traffic.get(dom) if not dist else None,
+        "traffic_source": (tsrc + " (ncu --set full, one launch)") if traffic and not dist else None,
         "peak_source": peaks["source"] + " (MEASURED_PEAKS.json hbm_gbs, copy)",
         "bytes_per_launch": kern[dom]["bytes_per_launch"],
         "share_of_step": round(kern[dom]["ms_total"] / prof_total, 4),

@@ -40,6 +40,14 @@ enum {
   ETC_PIVOT = 4
 };
 
+/* Preconditioner plugin kinds (reference tags "fct" | "jacobi" | "none",
+ * pipeline.py:114-132). */
+enum {
+  ETC_PRECOND_FCT = 0,    /* FctPreconditioner (preconditioner.py:253-282) */
+  ETC_PRECOND_JACOBI = 1, /* JacobiPreconditioner (preconditioner.py:324-330) */
+  ETC_PRECOND_NONE = 2    /* identity_apply (preconditioner.py:337-338)    */
+};
+
 /* Outcome of one solve (reference SolveReport, krylov.py:20-33). */
 typedef struct {
   int iterations;      /* == len(history) - 1                              */
@@ -101,6 +109,13 @@ int etc_solve(etc_plan* plan, double p_in, double p_out, double rtol, int max_it
  * solution vector (reference pcg() output, krylov.py:91) for
  * etc_get_solution. */
 int etc_keep_solution(etc_plan* plan, int keep);
+
+/* Select the preconditioner of the following etc_solve calls
+ * (_make_preconditioner, pipeline.py:125-132): ETC_PRECOND_FCT (default),
+ * ETC_PRECOND_JACOBI (r * 1/diag(A), diag in the accumulation order of
+ * operator_diagonal, tpfa.py:134-147) or ETC_PRECOND_NONE (z = r).  SSOR
+ * (SciPy SuperLU sweeps) is out of scope and has no kind. */
+int etc_set_precond(etc_plan* plan, int kind);
 
 /* Copy the solution vector p of the last solve (canonical layout); requires
  * etc_keep_solution(plan, 1) before the solve. */

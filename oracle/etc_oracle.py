@@ -333,11 +333,38 @@ def permute(kx, ky, kz, grid, axis: str):
     raise ValueError(axis)
 
 
+def operator_diagonal(fc, shape) -> np.ndarray:
+    """Diagonal of the 7-point operator, numpy accumulation order of
+    tpfa.py:134-147 (x faces from the left then the right, then y, z, then the
+    two Dirichlet layers)."""
+    tx, ty, tz, tin, tout = fc
+    d = np.zeros(shape)
+    d[:, :, 1:] += tx
+    d[:, :, :-1] += tx
+    d[:, 1:, :] += ty
+    d[:, :-1, :] += ty
+    d[1:, :, :] += tz
+    d[:-1, :, :] += tz
+    d[0] += tin
+    d[-1] += tout
+    return d
+
+
+def jacobi_inverse_diagonal(fc, shape) -> np.ndarray:
+    """JacobiPreconditioner._inv_diag = 1.0 / operator_diagonal (preconditioner.py:324-330)."""
+    return 1.0 / operator_diagonal(fc, shape)
+
+
 def homogenize(kx, ky, kz, grid, axis="z", p_in=1.0, p_out=0.0, rtol=1e-9,
-               ref_mode="opt", max_iter=1024, workers: int = 0, perturbed: bool = False) -> dict:
+               ref_mode="opt", max_iter=1024, workers: int = 0, perturbed: bool = False,
+               precond: str = "fct") -> dict:
     """kx, ky, kz: (nz, ny, nx) cubes; grid = (nx, ny, nz, lx, ly, lz).
     perturbed=True: reversed stencil association, bottom-up z elimination and
-    exactly rounded dots (same algorithm, different rounding)."""
+    exactly rounded dots (same algorithm, different rounding).
+    precond: "fct" (the FCT preconditioner), "jacobi" (r * 1/diag(A),
+    preconditioner.py:324-330) or "none" (a copy of r, :337-338), selected as
+    pipeline.py:114-132 does."""
+    precond_fct = globals()["precond"]
     kx, ky, kz, g = permute(kx, ky, kz, grid, axis)
     nx, ny, nz, lx, ly, lz = g
     s = (scale(kx, lx / nx), scale(ky, ly / ny), scale(kz, lz / nz))
@@ -347,10 +374,18 @@ def homogenize(kx, ky, kz, grid, axis="z", p_in=1.0, p_out=0.0, rtol=1e-9,
     tab = tables(nx, ny, nz, refs, kx.dtype.type)
     b = rhs(fc, kx.shape, p_in, p_out).reshape(-1)
     shape = kx.shape
+    if precond == "fct":
+        apply_m = lambda r: precond_fct(tab, r.reshape(shape), workers, perturbed).reshape(-1)  # noqa: E731
+    elif precond == "jacobi":
+        invd = jacobi_inverse_diagonal(fc, shape).reshape(-1)
+        apply_m = lambda r: r * invd  # noqa: E731
+    elif precond == "none":
+        apply_m = lambda r: r.copy()  # noqa: E731
+    else:
+        raise ValueError(f"unknown preconditioner {precond!r}")
     p, it, hist = pcg(
         lambda u: stencil(fc, u.reshape(shape), perturbed).reshape(-1),
-        lambda r: precond(tab, r.reshape(shape), workers, perturbed).reshape(-1),
-        b, rtol, max_iter, exact_dots=perturbed,
+        apply_m, b, rtol, max_iter, exact_dots=perturbed,
     )
     kappa = outflow_kappa(fc, p.reshape(shape), g, p_in, p_out)
     return {"iterations": it, "converged": hist[-1] <= rtol, "history": hist,

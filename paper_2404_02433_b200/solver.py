@@ -193,6 +193,10 @@ class DevicePlan:
     def keep_solution(self, keep: bool) -> None:
         _check(self.lib.etc_keep_solution(self._h, 1 if keep else 0), "etc_keep_solution")
 
+    def set_precond(self, kind: str) -> None:
+        """Preconditioner plugin of the next solves: "fct" | "jacobi" | "none"."""
+        _check(self.lib.etc_set_precond(self._h, _native.PRECOND_KINDS[kind]), "etc_set_precond")
+
     def solution(self):
         torch = _torch()
         g = self.canonical
@@ -273,11 +277,11 @@ def homogenize(
 
 
 def homogenize_with_solution(field, boundary: BoundaryConfig, rtol: float = 1e-9, ref_mode: str = "opt",
-                             max_iter: int = 1024, device=None):
+                             max_iter: int = 1024, device=None, precond: str = "fct"):
     """homogenize() that also returns the full potential p (canonical,
     z-oriented layout) as a CUDA tensor, like the reference's pcg()
     (krylov.py:91).  Costs one extra vector read+write per iteration."""
-    return _homogenize(field, boundary, rtol, "fct", ref_mode, "f64", 1.0, max_iter, device,
+    return _homogenize(field, boundary, rtol, precond, ref_mode, "f64", 1.0, max_iter, device,
                        keep_solution=True)
 
 
@@ -287,8 +291,9 @@ def _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_
     if ref_mode not in ("opt", "one"):
         raise ConfigError(f"ref mode must be opt or one, got {ref_mode!r}")
     kind, omega = _parse_precond(precond, omega)
-    if kind != "fct":
-        raise ConfigError(f"preconditioner {precond!r} is not implemented on the device (fct only)")
+    if kind == "ssor":
+        raise ConfigError("ssor (SciPy SuperLU triangular sweeps) is not implemented on the device; "
+                          "use fct, jacobi or none")
     if precision != "f64":
         raise ConfigError("the device solver computes in f64 only")
     if rtol <= 0.0:
@@ -307,6 +312,7 @@ def _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_
         refs = solve_reference_lp(stats) if ref_mode == "opt" else ones_reference(stats)
         plan.set_reference(refs)
         plan.keep_solution(keep_solution)
+        plan.set_precond(kind)
         prep = time.perf_counter() - t0
         t1 = time.perf_counter()
         info, history = plan.solve(boundary.p_in, boundary.p_out, rtol, max_iter)
@@ -328,13 +334,14 @@ def _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_
 
 
 def effective_tensor(field, rtol: float = 1e-9, p_in: float = 1.0, p_out: float = 0.0,
-                     ref_mode: str = "opt", max_iter: int = 1024, device=None, axes="xyz"):
+                     ref_mode: str = "opt", max_iter: int = 1024, device=None, axes="xyz",
+                     precond: str = "fct"):
     """Diagonal effective-conductivity tensor from one solve per load
     direction (the reference composes it from three homogenize() calls,
     pkg/tests/test_pipeline.py:54-58).  The field is uploaded once."""
     reports = {}
     for ax in axes:
-        reports[ax] = homogenize(field, BoundaryConfig(Axis(ax), p_in, p_out), rtol, "fct",
+        reports[ax] = homogenize(field, BoundaryConfig(Axis(ax), p_in, p_out), rtol, precond,
                                  ref_mode, "f64", 1.0, max_iter, device)
     kappa = np.array([reports[a].kappa_eff if a in reports else np.nan for a in "xyz"])
     return kappa, reports

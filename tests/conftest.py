@@ -35,3 +35,10 @@ def golden_precond():
     import json
 
     return json.loads((GOLDEN / "solves_precond.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def golden_channels():
+    import json
+
+    return json.loads((GOLDEN / "solves_channels.json").read_text())

@@ -3,6 +3,7 @@ golden vectors generated from /root/reference (tests/golden/make_golden.py)
 and the reference's own known-answer tests."""
 
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -163,3 +164,21 @@ def test_oracle_jacobi_none_match_reference(golden_precond):
         m = min(len(h), len(ref))
         big = ref[:m] > 1e-2
         assert np.all(np.abs(h[:m][big] - ref[:m][big]) <= 1e-8 * ref[:m][big])
+
+
+def test_oracle_channels_generator_and_solves(golden_channels):
+    """gen_channels (grid.py:287-319) bit for bit against the reference's
+    array, and the orthotropic channel solves (ref_mode opt and one, fct and
+    jacobi) against the reference runs up to 16^3."""
+    with np.load(Path(__file__).parent / "golden" / "channels_8x2.npz") as d:
+        for got, key in zip(O.channels(8, 2, 1.5), ("kx", "ky", "kz")):
+            assert np.array_equal(got.reshape(-1), d[key].reshape(-1)), key
+    for case in golden_channels:
+        n = case["n"]
+        if n > 16:
+            continue
+        kx, ky, kz = O.channels(case["cells_per_period"], case["periods"], case["psi"])
+        out = O.homogenize(kx, ky, kz, (n, n, n, 1.0, 1.0, 1.0), case["axis"], 1.0, 0.0, case["rtol"],
+                           ref_mode=case["ref_mode"], precond=case["precond"])
+        assert abs(out["iterations"] - case["iterations"]) <= 1, case["iterations"]
+        assert abs(out["kappa_eff"] - case["kappa_eff"]) <= 1e-8 * abs(case["kappa_eff"])

@@ -21,6 +21,9 @@ from .grid import (
     gen_fibres,
     gen_random_balls,
     linear_index,
+    read_vox,
+    VoxFormatError,
+    write_vox,
 )
 from .reference import (
     CoefficientStats,

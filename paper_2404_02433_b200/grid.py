@@ -13,6 +13,9 @@ from __future__ import annotations
 from dataclasses import dataclass
 from enum import Enum
 
+import struct
+from pathlib import Path
+
 import numpy as np
 
 
@@ -313,3 +316,73 @@ def gen_channels(cells_per_period: int, periods: int, psi: float, device=None,
     if as_numpy:
         k = [t.cpu().numpy() for t in k]
     return OrthotropicField(GridSpec(n, n, n), k[0], k[1], k[2], validate=False)
+
+
+# ----------------------------------------------------------------------------
+# ETCVOX01 container (reference grid.py:18-21, 28-34, 322-371)
+# ----------------------------------------------------------------------------
+
+VOX_MAGIC = b"ETCVOX01"
+_VOX_HEADER = struct.Struct("<8s3I3dB")  # magic, nx ny nz, lx ly lz, dtype code
+_VOX_DTYPE_BY_CODE = {0: np.dtype("<f8"), 1: np.dtype("<f4")}
+
+
+class VoxFormatError(ValueError):
+    """Malformed ETCVOX payload; carries the byte offset of the defect."""
+
+    def __init__(self, message: str, offset: int):
+        super().__init__(f"{message} (byte offset {offset})")
+        self.offset = offset
+
+
+def write_vox(field, destination, dtype=np.float64) -> None:
+    """Serialise a field (host arrays or CUDA tensors) to the single-file
+    little-endian ETCVOX container: header, then kx, ky, kz."""
+    dt = np.dtype(dtype)
+    code = {np.dtype(np.float64): 0, np.dtype(np.float32): 1}[dt]
+    g = field.grid
+    with open(Path(destination), "wb") as fh:
+        fh.write(_VOX_HEADER.pack(VOX_MAGIC, g.nx, g.ny, g.nz, g.lx, g.ly, g.lz, code))
+        for a in (field.kx, field.ky, field.kz):
+            if _is_tensor(a):
+                a = a.detach().cpu().numpy()
+            fh.write(np.ascontiguousarray(a, dtype=_VOX_DTYPE_BY_CODE[code]).tobytes())
+
+
+def read_vox(source, device=None) -> OrthotropicField:
+    """Parse an ETCVOX container with the reference's checks and error
+    offsets (truncated header, bad magic, unknown dtype code, bad dimensions,
+    payload size, first non-positive or non-finite entry).  f32 payloads are
+    widened to f64 (exact).  device: also place the arrays on that CUDA
+    device (one H2D copy; the solver then uses them in place)."""
+    raw = Path(source).read_bytes()
+    if len(raw) < _VOX_HEADER.size:
+        raise VoxFormatError("truncated header", len(raw))
+    magic, nx, ny, nz, lx, ly, lz, code = _VOX_HEADER.unpack_from(raw, 0)
+    if magic != VOX_MAGIC:
+        raise VoxFormatError(f"bad magic {magic!r}", 0)
+    if code not in _VOX_DTYPE_BY_CODE:
+        raise VoxFormatError(f"unknown dtype code {code}", _VOX_HEADER.size - 1)
+    try:
+        grid = GridSpec(int(nx), int(ny), int(nz), lx, ly, lz)
+    except ConfigError as exc:
+        raise VoxFormatError(f"bad dimensions: {exc}", 8) from exc
+    scalar = _VOX_DTYPE_BY_CODE[code]
+    count = grid.nx * grid.ny * grid.nz
+    expected = _VOX_HEADER.size + 3 * count * scalar.itemsize
+    if len(raw) != expected:
+        raise VoxFormatError(f"payload holds {len(raw)} bytes, expected {expected}", min(len(raw), expected))
+    arrays = []
+    for idx, name in enumerate(("kx", "ky", "kz")):
+        start = _VOX_HEADER.size + idx * count * scalar.itemsize
+        a = np.frombuffer(raw, dtype=scalar, count=count, offset=start)
+        bad = ~(np.isfinite(a) & (a > 0))
+        if np.any(bad):
+            first = int(np.argmax(bad))
+            raise VoxFormatError(f"non-positive {name} entry at cell {first}", start + first * scalar.itemsize)
+        arrays.append(a.astype(np.float64))
+    if device is not None:
+        import torch
+
+        arrays = [torch.from_numpy(a).to(device) for a in arrays]
+    return OrthotropicField(grid, *arrays, validate=False)

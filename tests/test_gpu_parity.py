@@ -104,7 +104,8 @@ def test_thomas_and_precond(golden_kernels):
 
 
 @pytest.mark.parametrize("dims", [(1, 1, 1), (3, 1, 1), (1, 1, 7), (9, 7, 5), (33, 17, 9),
-                                  (16, 16, 33), (64, 32, 40), (12, 20, 100), (128, 128, 128)])
+                                  (16, 16, 33), (64, 32, 40), (12, 20, 100), (128, 128, 128), (16, 16, 512),
+                                  (16, 8, 1024), (7, 5, 1024)])
 def test_precond_apply_back(dims):
     """A_ref M^-1 r = r with A_ref the reference operator as a stencil
     (reference_system, preconditioner.py:143-164; criterion 3)."""

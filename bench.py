@@ -47,15 +47,17 @@ def metric_for(args) -> str:
 KCLASS = ["stencil", "update_fwd2d", "fwd2d", "zsolve", "unused", "inv2d", "setup"]
 
 
-def bytes_per_cell(wfuse: bool) -> dict:
+def bytes_per_cell(wfuse: bool, phases: bool = False) -> dict:
     """Algorithmic (compulsory) HBM bytes per cell per launch, f64.
 
     wfuse (single-GPU square planes, the default): the inverse transform
     builds the search direction w = z + beta w_old itself, so the stencil
-    reads w instead of z and w_old and writes only q."""
+    reads w instead of z and w_old and writes only q.  phases (the field has
+    at most 16 distinct conductivity triples, as every benchmark field does):
+    a one-byte phase index replaces the three face arrays."""
     if wfuse:
         return {
-            "stencil": 40,  # w, tx, ty, tz read; q written
+            "stencil": 17 if phases else 40,  # w, idx (or tx, ty, tz) read; q written
             "update_fwd2d": 32,  # r, q read; r, t(=q) written; x+y DCT-II fused per plane
             "fwd2d": 16, "zsolve": 16,
             "inv2d": 24,  # t, w_old read; w written (16 on the first launch of a solve: w = z)
@@ -299,7 +301,8 @@ def run_b200(args, rank, world, local_rank):
     N = n ** 3 // world  # cells per rank per launch
     wfuse = (not dist and not args.slab and os.environ.get("ETC_WFUSE", "1") != "0" and n >= 128
              and n & (n - 1) == 0)
-    bpc = bytes_per_cell(wfuse)
+    phases = wfuse and os.environ.get("ETC_PHASES", "1") != "0"  # the bench field has two phases
+    bpc = bytes_per_cell(wfuse, phases)
     peaks = load_peaks()
     kern = {}
     for i, name in enumerate(KCLASS):

@@ -443,3 +443,26 @@ def test_vox_file_to_device_solve():
     a = P.homogenize(f, bc, 1e-8)
     b = P.homogenize(P.gen_center_ball(8, 10.0), bc, 1e-8)
     assert (a.iterations, a.relative_residuals, a.kappa_eff) == (b.iterations, b.relative_residuals, b.kappa_eff)
+
+
+def test_phase_indexed_stencil_is_bitwise_equal(monkeypatch):
+    """Few-phase fields (<= 16 distinct (s_x, s_y, s_z)): the stencil looks the
+    faces up from a per-cell phase index and PH_MAX^2 tables built with the
+    same harm(); the solve is bit-identical to the stored-faces one.  An
+    orthotropic two-phase lattice and a random-inclusion pack, plus a field
+    with too many phases (falls back)."""
+    bc = P.BoundaryConfig(P.Axis("x"), 1.0, 0.0)
+    rng = np.random.default_rng(3)
+    many = np.exp(rng.uniform(-3, 3, 128 ** 3))
+    fields = [P.gen_random_balls(128, 40, 0.05, 0.15, 100.0, 11), P.gen_channels(16, 8, 2.0),
+              P.OrthotropicField(P.GridSpec(128, 128, 128), many, many, many)]
+    for f in fields:
+        out = []
+        for env in ("1", "0"):
+            monkeypatch.setenv("ETC_PHASES", env)
+            P.release_plans()
+            r = P.homogenize(f, bc, 1e-8)
+            out.append((r.iterations, list(r.relative_residuals), r.kappa_eff))
+        assert out[0] == out[1]
+    monkeypatch.delenv("ETC_PHASES", raising=False)
+    P.release_plans()

@@ -4,9 +4,9 @@ Same flags, report JSON schema (`report_to_dict`, pipeline.py:250-280),
 residual CSV (`write_history`, pipeline.py:290-295) and exit codes as the
 reference CLI (cli.py:1-5, 165-186, 300-323): 0 success, 1 non-convergence
 or breakdown, 2 usage / configuration error, 3 I/O or file-format error.
-The study subcommands (convergence, compare, channels, precision, bench,
-oracle) are experiment drivers around the hot path and stay with the
-reference.
+The study subcommands (convergence, compare, channels, precision, bench)
+and the verification-suite runner are experiment drivers around the hot
+path and stay with the reference.
 
     python -m paper_2404_02433_b200 generate --config random-balls --preset a --n 128 -o f.vox
     python -m paper_2404_02433_b200 solve f.vox --axis z --rtol 1e-6 --report r.json --history h.csv

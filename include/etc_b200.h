@@ -160,13 +160,20 @@ int etc_profile_read(etc_plan* plan, double ms[8], long long counts[8], int rese
 int etc_slab_create(etc_plan** out, int nx, int ny, int nzg, int k0, int nzl, int nranks, int rank,
                     double lx, double ly, double lz, void* stream);
 int etc_slab_load(etc_plan* plan, const double* kx, const double* ky, const double* kz, int on_device);
-/* which: 0..2 s_x,s_y,s_z, 3 z; plane -1..nzl (halo planes -1 and nzl);
+/* which: 0..2 s_x,s_y,s_z, 3 z, 4 w (fused path); plane -1..nzl (halo planes -1 and nzl);
  * to_ext != 0 copies plan -> ext, else ext -> plan (device pointers). */
 int etc_slab_plane(etc_plan* plan, int which, int plane, double* ext, int to_ext);
 int etc_slab_init(etc_plan* plan, double p_in, double p_out, double rtol, int max_iter, double* xbuf);
 int etc_slab_run(etc_plan* plan, int stage, int arg, double* ext);
 /* ctl state + history; info->pad_ carries the device `done` flag. */
 int etc_slab_status(etc_plan* plan, etc_solve_info* info, double* hist_host);
+
+/* 1 if this slab plan runs the fused search-direction path (square
+ * power-of-two planes): the inverse stage builds w (arg 1: w = z, arg 2:
+ * p += alpha w_old on the outflow plane, w = z + beta w_old), the stencil
+ * stage reads w, and the host exchanges w halo planes (etc_slab_plane
+ * which = 4) instead of z (which = 3) after the inverse. */
+int etc_slab_fused(etc_plan* plan);
 
 /* Voxelise gen_random_balls / gen_center_ball (grid.py:230-275) on the device:
  * balls = count x (cx, cy, cz, r) drawn on the host; out = n^3 cube of

@@ -25,7 +25,7 @@ EXPORTS = (
     "etc_apply_operator", "etc_dct2_xy", "etc_dct3_xy", "etc_thomas",
     "etc_apply_precond", "etc_build_rhs", "etc_profile", "etc_profile_read",
     "etc_voxelize_balls", "etc_voxelize_fibres", "etc_fill_channels", "etc_slab_create", "etc_slab_load", "etc_slab_plane",
-    "etc_slab_init", "etc_slab_run", "etc_slab_status",
+    "etc_slab_init", "etc_slab_run", "etc_slab_status", "etc_slab_fused",
 )
 
 
@@ -87,6 +87,7 @@ _SIGS = {
     "etc_slab_init": (_I, [_P, _D, _D, _D, _I, _P]),
     "etc_slab_run": (_I, [_P, _I, _I, _P]),
     "etc_slab_status": (_I, [_P, C.POINTER(SolveInfo), _DP]),
+    "etc_slab_fused": (_I, [_P]),
 }
 
 

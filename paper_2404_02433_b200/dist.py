@@ -219,6 +219,9 @@ class CudaSlabOps:
         _check(self.lib.etc_slab_init(self._h, float(p_in), float(p_out), float(rtol), int(max_iter),
                                       xbuf.data_ptr()), "etc_slab_init")
 
+    def fused(self) -> bool:
+        return bool(self.lib.etc_slab_fused(self._h))
+
     def status(self, max_iter):
         info = _native.SolveInfo()
         hist = np.empty(max_iter + 1, dtype=np.float64)
@@ -286,7 +289,11 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
     send = ops.new(nloc)
     recv = ops.new(nloc)
 
-    def zsolve_and_back():
+    # fused path (square power-of-two planes): the inverse stage builds the
+    # search direction w itself, so the w halo planes move instead of z
+    fused = ops.fused()
+
+    def zsolve_and_back(first):
         ops.run(SLAB_PACK, 0, send)
         comm.alltoall(recv, send)
         ops.run(SLAB_ZSOLVE, 0, recv)
@@ -294,14 +301,14 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
         ops.run(SLAB_UNPACK, 0, send)
         comm.allreduce(xbuf[4:5])
         ops.run(SLAB_FINALIZE, FIN_THOMAS)
-        ops.run(SLAB_INVERSE)
-        _exchange_planes(ops, comm, 3, nzl)
+        ops.run(SLAB_INVERSE, 1 if first else 2)
+        _exchange_planes(ops, comm, 4 if fused else 3, nzl)
 
     ops.init(p_in, p_out, rtol, max_iter, xbuf)
     ops.run(SLAB_NORMB)
     comm.allreduce(xbuf[3:4])
     ops.run(SLAB_FINALIZE, FIN_NORMB)
-    zsolve_and_back()
+    zsolve_and_back(True)
     it = 0
     done = False
     while not done and it < max_iter:
@@ -312,7 +319,7 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
         ops.run(SLAB_UPDATE)
         comm.allreduce(xbuf[3:4])
         ops.run(SLAB_FINALIZE, FIN_UPDATE)
-        zsolve_and_back()
+        zsolve_and_back(False)
         if it % check_every == 0 or it == max_iter:
             info, _ = ops.status(max_iter)
             done = info.pad_ != 0

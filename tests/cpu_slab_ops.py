@@ -25,12 +25,16 @@ EPS = 2.220446049250313e-16
 
 
 class CpuSlabOps:
-    def __init__(self, nx, ny, nzg, k0, nzl, size, rank, lx, ly, lz):
+    def __init__(self, nx, ny, nzg, k0, nzl, size, rank, lx, ly, lz, fused=False):
         self.nx, self.ny, self.nzg, self.k0, self.nzl = nx, ny, nzg, k0, nzl
         self.size, self.rank = size, rank
         self.lx, self.ly, self.lz = lx, ly, lz
         self.s = None
         self.ctl = None
+        self._fused = fused  # the inverse builds w (etc_slab_fused)
+
+    def fused(self):
+        return self._fused
 
     # -- buffers ------------------------------------------------------------
     def new(self, n):
@@ -46,9 +50,10 @@ class CpuSlabOps:
             self.s.append(ext)
         self.z = np.zeros((nzl + 2, ny, nx))
         self.w = [np.zeros((nzl + 2, ny, nx)), np.zeros((nzl + 2, ny, nx))]
+        self.wf = np.zeros((nzl + 2, ny, nx))  # fused path: the search direction, with halos
 
     def _buf(self, which):
-        return self.s[which] if which <= 2 else self.z
+        return self.s[which] if which <= 2 else (self.z if which == 3 else self.wf)
 
     def get_plane(self, which, plane):
         return torch.from_numpy(self._buf(which)[plane + 1].reshape(-1).copy())
@@ -156,15 +161,18 @@ class CpuSlabOps:
         c = self.ctl
         if c.done:
             return
-        wn, wo = self.w[it & 1], self.w[(it - 1) & 1]
-        if it == 1:
-            wn[:] = self.z
+        if self._fused:
+            u = self.wf
         else:
-            wn[:] = self.z + c.beta * wo
-            kl = self.nzg - 1 - self.k0
-            if 0 <= kl < self.nzl:
-                self.p[kl] = self.p[kl] + c.alpha * wo[kl + 1]
-        u = wn
+            wn, wo = self.w[it & 1], self.w[(it - 1) & 1]
+            if it == 1:
+                wn[:] = self.z
+            else:
+                wn[:] = self.z + c.beta * wo
+                kl = self.nzg - 1 - self.k0
+                if 0 <= kl < self.nzl:
+                    self.p[kl] = self.p[kl] + c.alpha * wo[kl + 1]
+            u = wn
         nzl = self.nzl
         q = np.zeros((nzl, self.ny, self.nx))
         core = u[1:-1]
@@ -221,15 +229,25 @@ class CpuSlabOps:
         a = ext.numpy().reshape(self.size, self.nzl, nyl, self.nx)
         self.t = np.concatenate([a[s] for s in range(self.size)], axis=1)
 
-    def _stage9(self, arg, ext):  # inverse transform
-        if self.ctl.done:
+    def _stage9(self, arg, ext):  # inverse transform (fused: builds w, arg 1 first / 2 update)
+        c = self.ctl
+        if c.done:
             return
         self.z[1:-1] = O.fct_backward(self.t)
+        if self._fused:
+            if arg == 1:
+                self.wf[1:-1] = self.z[1:-1]
+            else:
+                kl = self.nzg - 1 - self.k0
+                if 0 <= kl < self.nzl:
+                    self.p[kl] = self.p[kl] + c.alpha * self.wf[kl + 1]
+                self.wf[1:-1] = self.z[1:-1] + c.beta * self.wf[1:-1]
 
     def _stage10(self, it, ext):  # final p update on the outflow plane
         kl = self.nzg - 1 - self.k0
+        w = self.wf if self._fused else self.w[it & 1]
         if it >= 1 and 0 <= kl < self.nzl:
-            self.p[kl] = self.p[kl] + self.ctl.alpha * self.w[it & 1][kl + 1]
+            self.p[kl] = self.p[kl] + self.ctl.alpha * w[kl + 1]
 
     def _stage11(self, arg, ext):  # outflow flux
         kl = self.nzg - 1 - self.k0

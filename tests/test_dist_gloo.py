@@ -66,7 +66,7 @@ def _primitives(rank, size, port, q):
             td.destroy_process_group()
 
 
-def _solve(rank, size, port, q, n, C, axis):
+def _solve(rank, size, port, q, n, C, axis, fused=False):
     try:
         _init(rank, size, port)
         from cpu_slab_ops import CpuSlabOps
@@ -78,7 +78,7 @@ def _solve(rank, size, port, q, n, C, axis):
         kx, ky, kz, g = O.permute(k, k, k, (n, n, n, 1.0, 1.0, 1.0), axis)
         k0, nzl = slab_bounds(g[2], size, rank)
         sl = lambda a: torch.from_numpy(np.ascontiguousarray(a[k0:k0 + nzl]).reshape(-1))
-        ops = CpuSlabOps(g[0], g[1], g[2], k0, nzl, size, rank, g[3], g[4], g[5])
+        ops = CpuSlabOps(g[0], g[1], g[2], k0, nzl, size, rank, g[3], g[4], g[5], fused=fused)
         t = sl(kx)
         rep = slab_solve(ops, comm, t, t, t, g, 1.0, 0.0, 1e-8)
         q.put((rank, (rep.iterations, rep.kappa_eff, rep.relative_residuals), None))
@@ -110,14 +110,16 @@ def test_comm_primitives(size):
         assert ok, (rank, err)
 
 
-@pytest.mark.parametrize("size,n,C,axis", [(2, 16, 100.0, "z"), (4, 16, 10.0, "x"), (2, 24, 100.0, "y")])
-def test_slab_solve_matches_single_process(size, n, C, axis):
+@pytest.mark.parametrize("size,n,C,axis,fused", [(2, 16, 100.0, "z", False), (4, 16, 10.0, "x", False),
+                                                 (2, 24, 100.0, "y", False), (2, 16, 100.0, "z", True),
+                                                 (4, 16, 10.0, "y", True)])
+def test_slab_solve_matches_single_process(size, n, C, axis, fused):
     sys.path.insert(0, str(ROOT))
     from oracle import etc_oracle as O
 
     k = O.random_balls(n, 40, 0.05, 0.15, C, 11)
     ref = O.homogenize(k, k, k, (n, n, n, 1.0, 1.0, 1.0), axis, 1.0, 0.0, 1e-8)
-    res = _spawn(_solve, size, n, C, axis)
+    res = _spawn(_solve, size, n, C, axis, fused)
     for rank, out, err in res:
         assert err is None, err
         it, kappa, hist = out

@@ -250,6 +250,24 @@ def test_orthotropic_and_anisotropic_grid():
         assert abs(rep.kappa_eff - out["kappa_eff"]) <= 1e-8 * abs(out["kappa_eff"])
 
 
+@pytest.mark.parametrize("dims,axis", [((128, 128, 100), "z"), ((100, 128, 128), "x"), ((256, 96, 256), "y")])
+def test_fused_path_on_mixed_shapes(dims, axis):
+    """Shapes whose canonical plane is square and power of two while the
+    slab is not (the fused kernels with the runtime-size z-solve), and the
+    reverse (the runtime-size transforms): a two-phase field, every path
+    against the oracle at the same inputs."""
+    nx, ny, nz = dims
+    rng = np.random.default_rng(nx + ny + nz)
+    k3 = np.where(rng.random((nz, ny, nx)) < 0.3, 50.0, 1.0)
+    g = P.GridSpec(nx, ny, nz, 1.0, 1.0, 1.0)
+    k = k3.reshape(-1)
+    rep = P.homogenize(P.OrthotropicField(g, k, k, k), P.BoundaryConfig(P.Axis(axis), 1.0, 0.0), 1e-7)
+    out = O.homogenize(k3, k3, k3, (nx, ny, nz, 1.0, 1.0, 1.0), axis, 1.0, 0.0, 1e-7)
+    assert abs(rep.iterations - out["iterations"]) <= 1, (rep.iterations, out["iterations"])
+    assert abs(rep.kappa_eff - out["kappa_eff"]) <= 1e-8 * abs(out["kappa_eff"])
+    assert _hist_dev(rep.relative_residuals, out["history"]) <= 1e-8
+
+
 def test_homogeneous_one_iteration():
     # matched reference -> exact preconditioner -> 1 iteration (test_pipeline.py:62-65)
     g = P.GridSpec(8, 6, 10)

@@ -293,19 +293,26 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
     # search direction w itself, so the w halo planes move instead of z
     fused = ops.fused()
 
+    # on the fused path the forward transform writes its spectrum straight
+    # into the all-to-all send buffer and the inverse reads it back from there
+    # (pack / unpack fused into the transforms)
+    spec = send if fused else None
+
     def zsolve_and_back(first):
-        ops.run(SLAB_PACK, 0, send)
+        if not fused:
+            ops.run(SLAB_PACK, 0, send)
         comm.alltoall(recv, send)
         ops.run(SLAB_ZSOLVE, 0, recv)
         comm.alltoall(send, recv)
-        ops.run(SLAB_UNPACK, 0, send)
+        if not fused:
+            ops.run(SLAB_UNPACK, 0, send)
         comm.allreduce(xbuf[4:5])
         ops.run(SLAB_FINALIZE, FIN_THOMAS)
-        ops.run(SLAB_INVERSE, 1 if first else 2)
+        ops.run(SLAB_INVERSE, 1 if first else 2, spec)
         _exchange_planes(ops, comm, 4 if fused else 3, nzl)
 
     ops.init(p_in, p_out, rtol, max_iter, xbuf)
-    ops.run(SLAB_NORMB)
+    ops.run(SLAB_NORMB, 0, spec)
     comm.allreduce(xbuf[3:4])
     ops.run(SLAB_FINALIZE, FIN_NORMB)
     zsolve_and_back(True)
@@ -316,7 +323,7 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
         ops.run(SLAB_STENCIL, it)
         comm.allreduce(xbuf[0:3])
         ops.run(SLAB_FINALIZE, FIN_STENCIL)
-        ops.run(SLAB_UPDATE)
+        ops.run(SLAB_UPDATE, 0, spec)
         comm.allreduce(xbuf[3:4])
         ops.run(SLAB_FINALIZE, FIN_UPDATE)
         zsolve_and_back(False)

@@ -116,9 +116,21 @@ class CpuSlabOps:
             self.r[-1] += (2.0 * sz[-1]) * p_out
         self.p = np.zeros_like(self.r)
 
-    def _stage2(self, arg, ext):  # ||b|| + first transform
+    def _pack(self, ext):
+        nyl = self.ny // self.size
+        blocks = [self.t[:, r * nyl:(r + 1) * nyl, :] for r in range(self.size)]
+        ext.copy_(torch.from_numpy(np.concatenate([b.reshape(-1) for b in blocks])))
+
+    def _unpack(self, ext):
+        nyl = self.ny // self.size
+        a = ext.numpy().reshape(self.size, self.nzl, nyl, self.nx)
+        self.t = np.concatenate([a[s] for s in range(self.size)], axis=1)
+
+    def _stage2(self, arg, ext):  # ||b|| + first transform (fused: written packed into ext)
         self.xbuf[3] = float(np.sum(self.r * self.r))
         self.t = O.fct_forward(self.r)
+        if ext is not None:
+            self._pack(ext)
 
     def _stage3(self, stage, ext):  # finalize
         c, x = self.ctl, self.xbuf.numpy()
@@ -199,17 +211,17 @@ class CpuSlabOps:
         self.xbuf[1] = float(np.sum(q * q))
         self.xbuf[2] = float(np.sum(core * core))
 
-    def _stage5(self, arg, ext):  # r -= alpha q; ||r||; transform
+    def _stage5(self, arg, ext):  # r -= alpha q; ||r||; transform (fused: written packed into ext)
         if self.ctl.done:
             return
         self.r = self.r - self.ctl.alpha * self.q
         self.xbuf[3] = float(np.sum(self.r * self.r))
         self.t = O.fct_forward(self.r)
+        if ext is not None:
+            self._pack(ext)
 
     def _stage6(self, arg, ext):  # pack
-        nyl = self.ny // self.size
-        blocks = [self.t[:, r * nyl:(r + 1) * nyl, :] for r in range(self.size)]
-        ext.copy_(torch.from_numpy(np.concatenate([b.reshape(-1) for b in blocks])))
+        self._pack(ext)
 
     def _stage7(self, arg, ext):  # z-solve on the pencil
         if self.ctl.done:
@@ -225,14 +237,14 @@ class CpuSlabOps:
         ext.copy_(torch.from_numpy(x.reshape(-1)))
 
     def _stage8(self, arg, ext):  # unpack
-        nyl = self.ny // self.size
-        a = ext.numpy().reshape(self.size, self.nzl, nyl, self.nx)
-        self.t = np.concatenate([a[s] for s in range(self.size)], axis=1)
+        self._unpack(ext)
 
-    def _stage9(self, arg, ext):  # inverse transform (fused: builds w, arg 1 first / 2 update)
+    def _stage9(self, arg, ext):  # inverse transform (fused: builds w, arg 1 first / 2 update; reads ext)
         c = self.ctl
         if c.done:
             return
+        if ext is not None:
+            self._unpack(ext)
         self.z[1:-1] = O.fct_backward(self.t)
         if self._fused:
             if arg == 1:

@@ -340,7 +340,11 @@ def run_b200(args, rank, world, local_rank):
     # end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        kh = field.kx.cpu().numpy()
+        # the step's input lives in pinned host memory (the contract's e2e
+        # setup); every step copies it to the device inside the timed region
+        kh_t = torch.empty(n ** 3, dtype=torch.float64, pin_memory=True)
+        kh_t.copy_(field.kx.reshape(-1).cpu())
+        kh = kh_t.numpy()
         hostgrid = field.grid
         torch.cuda.synchronize()
         t_e2e = []
@@ -359,7 +363,8 @@ def run_b200(args, rank, world, local_rank):
         e2e = {"value": round(statistics.mean(t_e2e), 4), "unit": "s",
                "h2d_bytes_per_step": int(kh.nbytes if not dist else 3 * kh.nbytes // world),
                "d2h_bytes_per_step": int(sum(8 * (r.iterations + 1) + 8 for r in rp.values())),
-               "samples": len(t_e2e), "api": "paper_2404_02433_b200.effective_tensor(host numpy field)"}
+               "samples": len(t_e2e),
+               "api": "paper_2404_02433_b200.effective_tensor(numpy field in pinned host memory)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

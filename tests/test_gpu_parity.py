@@ -512,13 +512,17 @@ def test_phase_indexed_operator_bitwise(monkeypatch, which):
          "channels": lambda: P.gen_channels(8, 8, 2.0),
          "fibres": lambda: P.gen_fibres(n, 24, 0.04, 0.08, 1000.0, 5, axis="y")}[which]()
     u = np.random.default_rng(7).standard_normal(n ** 3)
-    out = []
+    out, stats = [], []
     for env in ("1", "0"):
         monkeypatch.setenv("ETC_PHASES", env)
         P.release_plans()
         ds = P.DeviceSystem(f, P.BoundaryConfig(P.Axis("x"), 1.0, 0.0))
         out.append(_cpu(ds.apply_operator(u)))
+        stats.append([v for pair in ds.stats.groups().values() for v in pair])
         del ds
     monkeypatch.delenv("ETC_PHASES", raising=False)
     P.release_plans()
     assert np.array_equal(out[0], out[1])
+    # coefficient statistics from the face tables and the phase pairs that
+    # meet == the exact min/max over every face (k_stats), bit for bit
+    assert stats[0] == stats[1]

@@ -261,6 +261,10 @@ def run_b200(args, rank, world, local_rank):
         return tot_ms, tot_cnt
 
     prof_read()  # reset counters
+    # per-kernel device times are taken live over the timed region: CUDA
+    # events around every launch on the plan stream (read after the region)
+    for h in handles():
+        lib.etc_profile(h, 1)
 
     clocks = Clocks(local_rank)
     if dist:
@@ -279,7 +283,9 @@ def run_b200(args, rank, world, local_rank):
     if dist:
         td.barrier()
     ms_total = e0.elapsed_time(e1)
-    _, cnts = prof_read()
+    for h in handles():
+        lib.etc_profile(h, 0)
+    pms, cnts = prof_read()
     launches = int(sum(cnts))
     if dist:
         t = torch.tensor([ms_total], device=dev)
@@ -289,15 +295,8 @@ def run_b200(args, rank, world, local_rank):
     iters = {a: reps[a].iterations for a in axes}
     total_iters = sum(iters.values())
 
-    # one profiled step: per-kernel device time (events on the plan stream)
-    for h in handles():
-        lib.etc_profile(h, 1)
-    step()
-    for h in handles():
-        lib.etc_profile(h, 0)
-    pms, pcnt = prof_read()
-    for i in range(8):
-        ms8[i], cnt8[i] = pms[i], pcnt[i]
+    kms = [pms[i] / args.steps for i in range(8)]  # per-kernel totals per timed step
+    kcnt = [cnts[i] / args.steps for i in range(8)]
     N = n ** 3 // world  # cells per rank per launch
     wfuse = (not dist and not args.slab and os.environ.get("ETC_WFUSE", "1") != "0" and n >= 128
              and n & (n - 1) == 0)
@@ -306,14 +305,14 @@ def run_b200(args, rank, world, local_rank):
     peaks = load_peaks()
     kern = {}
     for i, name in enumerate(KCLASS):
-        if cnt8[i] == 0:
+        if kcnt[i] == 0:
             continue
-        avg = ms8[i] / cnt8[i]
-        d = {"ms_total": round(ms8[i], 4), "launches": int(cnt8[i]), "ms_avg": round(avg, 5)}
+        avg = kms[i] / kcnt[i]
+        d = {"ms_total": round(kms[i], 4), "launches": int(round(kcnt[i])), "ms_avg": round(avg, 5)}
         if name in bpc:
             b = bpc[name] * N
             if wfuse and name == "inv2d":  # first launch of each solve writes w = z (16 B/cell)
-                b = (16 * N * len(axes) + 24 * N * (cnt8[i] - len(axes))) / cnt8[i]
+                b = (16 * N * len(axes) + 24 * N * (kcnt[i] - len(axes))) / kcnt[i]
             gbs = b / (avg * 1e-3) / 1e9
             d.update(bytes_per_launch=int(b), gbs=round(gbs, 1), frac=round(gbs / peaks["hbm_gbs"], 4))
         kern[name] = d

@@ -175,6 +175,29 @@ int etc_slab_status(etc_plan* plan, etc_solve_info* info, double* hist_host);
  * which = 4) instead of z (which = 3) after the inverse. */
 int etc_slab_fused(etc_plan* plan);
 
+/* Peer exchange (fused all-to-all over peer memory): 1 if this slab plan
+ * can run it (fused path, exact-fit z-solve on the pencil). */
+int etc_slab_p2p_ok(etc_plan* plan);
+/* The plan's exchange buffers (device, nzl*ny*nx doubles each, allocated on
+ * first request): which 0 = pencil (recv) buffer, 1 = return buffer. */
+int etc_slab_xbuf(etc_plan* plan, int which, double** out);
+/* Every rank's pencil and return buffers as pointers valid in this process
+ * (own, same-process, or CUDA-IPC-opened), nranks entries each; NULL turns
+ * the peer exchange off.  With peers set, SLAB_NORMB/SLAB_UPDATE store the
+ * spectrum into the destination ranks' pencil buffers and SLAB_ZSOLVE stores
+ * its rows into the owners' return buffers (no all-to-all); the host's
+ * following scalar all-reduce is the barrier. */
+int etc_slab_set_peers(etc_plan* plan, double* const* recv_peers, double* const* back_peers);
+/* Device address of plane `plane` (-1..nzl) of buffer `which` (as
+ * etc_slab_plane): the target of the peers' halo-plane stores. */
+int etc_slab_plane_ptr(etc_plan* plan, int which, int plane, double** out);
+/* CUDA IPC helpers for multi-process ranks: the 64-byte handle of the plan
+ * allocation holding dev_ptr and dev_ptr's byte offset in it; open / close a
+ * peer's handle (the opened base + offset is the peer's pointer). */
+int etc_ipc_handle(etc_plan* plan, const void* dev_ptr, void* handle_out, size_t* offset_out);
+int etc_ipc_open(const void* handle_in, void** dev_ptr);
+int etc_ipc_close(void* dev_ptr);
+
 /* Voxelise gen_random_balls / gen_center_ball (grid.py:230-275) on the device:
  * balls = count x (cx, cy, cz, r) drawn on the host; out = n^3 cube of
  * kappa_inc inside any ball, 1.0 elsewhere (bit-identical membership test). */

@@ -82,6 +82,27 @@ class TorchComm:
     def alltoall(self, out, inp):
         self.td.all_to_all_single(out, inp, group=self.group)
 
+    def barrier(self):
+        # peer stores were issued on the current stream: complete them first
+        # (a gloo barrier is host-side)
+        _torch().cuda.current_stream().synchronize()
+        self.td.barrier(group=self.group)
+
+    def share_pointers(self, ops, ptrs):
+        """Every rank's device pointers `ptrs` as pointers valid in this
+        process: own ones as they are, the peers' opened through CUDA IPC
+        (handle of the plan allocation + byte offset)."""
+        mine = [ops.ipc_handle(p) for p in ptrs]
+        allh = [None] * self.size
+        self.td.all_gather_object(allh, mine, group=self.group)
+        out = []
+        for r, hs in enumerate(allh):
+            if r == self.rank:
+                out.append(list(ptrs))
+            else:
+                out.append([_ipc_open(h, off) for h, off in hs])
+        return out
+
     def neighbours(self, lo, hi, recv_lo, recv_hi):
         """send lo -> rank-1 (its upper halo), hi -> rank+1 (its lower halo);
         receive rank-1's hi into recv_lo and rank+1's lo into recv_hi."""
@@ -94,6 +115,19 @@ class TorchComm:
         if ops:
             for req in td.batch_isend_irecv(ops):
                 req.wait()
+
+
+_IPC_OPEN = {}
+
+
+def _ipc_open(handle: bytes, offset: int) -> int:
+    """Open a peer's allocation once per process; base + offset."""
+    base = _IPC_OPEN.get(handle)
+    if base is None:
+        ptr = C.c_void_p()
+        _check(_native.lib().etc_ipc_open(C.c_char_p(handle), C.byref(ptr)), "etc_ipc_open")
+        base = _IPC_OPEN[handle] = int(ptr.value)
+    return base + offset
 
 
 class _ThreadHub:
@@ -123,6 +157,17 @@ class ThreadComm:
         if torch.cuda.is_available():
             torch.cuda.synchronize()
         self.hub.barrier.wait()
+
+    def barrier(self):
+        self._sync()
+
+    def share_pointers(self, ops, ptrs):
+        """One process: the ranks' device pointers are valid as they are."""
+        self.hub.slots[self.rank] = list(ptrs)
+        self._sync()
+        out = [list(x) for x in self.hub.slots]
+        self._sync()
+        return out
 
     def allreduce(self, t, op: str = "sum"):
         self.hub.slots[self.rank] = t
@@ -222,6 +267,34 @@ class CudaSlabOps:
     def fused(self) -> bool:
         return bool(self.lib.etc_slab_fused(self._h))
 
+    # -- peer exchange (fused all-to-all over peer memory) ---------------------
+    def p2p_ok(self) -> bool:
+        return bool(self.lib.etc_slab_p2p_ok(self._h))
+
+    def xbuf(self, which: int) -> int:
+        ptr = C.c_void_p()
+        _check(self.lib.etc_slab_xbuf(self._h, which, C.byref(ptr)), "etc_slab_xbuf")
+        return int(ptr.value)
+
+    def plane_ptr(self, which: int, plane: int) -> int:
+        ptr = C.c_void_p()
+        _check(self.lib.etc_slab_plane_ptr(self._h, which, plane, C.byref(ptr)), "etc_slab_plane_ptr")
+        return int(ptr.value)
+
+    def ipc_handle(self, ptr: int):
+        buf = C.create_string_buffer(64)
+        off = C.c_size_t()
+        _check(self.lib.etc_ipc_handle(self._h, C.c_void_p(ptr), buf, C.byref(off)), "etc_ipc_handle")
+        return bytes(buf.raw), int(off.value)
+
+    def set_peers(self, recv_ptrs, back_ptrs):
+        arr = C.c_void_p * len(recv_ptrs)
+        _check(self.lib.etc_slab_set_peers(self._h, arr(*recv_ptrs), arr(*back_ptrs)), "etc_slab_set_peers")
+
+    def put_plane(self, which: int, plane: int, dst_ptr: int):
+        """Copy this rank's plane into a (peer) device address."""
+        _check(self.lib.etc_slab_plane(self._h, which, plane, C.c_void_p(dst_ptr), 1), "etc_slab_plane")
+
     def status(self, max_iter):
         info = _native.SolveInfo()
         hist = np.empty(max_iter + 1, dtype=np.float64)
@@ -255,16 +328,51 @@ def _exchange_planes(ops, comm, which: int, nzl: int):
 
 
 def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_mode="opt",
-               max_iter=1024, check_every=1) -> SolveReport:
+               max_iter=1024, check_every=1, p2p=None) -> SolveReport:
     """PCG on this rank's z-slab of the canonical field (kx, ky, kz: local
     planes, x-fastest).  grid = (nx, ny, nzg, lx, ly, lz), the canonical
-    global grid.  Every rank returns the same report."""
+    global grid.  Every rank returns the same report.
+
+    p2p (default: ETC_P2P=1 in the environment): the pencil all-to-alls are
+    fused into the producing kernels over peer memory (the forward transform
+    stores into the destination ranks' pencil buffers, the z-solve into the
+    owners' return buffers; halo planes are stored into the neighbours' halo
+    planes), where the plan supports it (etc_slab_p2p_ok) and the comm can
+    share device pointers (same process, or CUDA IPC)."""
     nx, ny, nzg, lx, ly, lz = grid
     nzl = nzg // comm.size
     iso = kx is ky and ky is kz
     ops.load(kx, ky, kz)
-    for which in ((2,) if iso else (0, 1, 2)):
-        _exchange_planes(ops, comm, which, nzl)
+    if p2p is None:
+        import os
+
+        p2p = os.environ.get("ETC_P2P", "0") == "1"
+    use_p2p = bool(p2p) and hasattr(comm, "share_pointers") and hasattr(ops, "p2p_ok") and ops.p2p_ok()
+    if p2p and comm.size > 1:  # every rank must agree
+        t = ops.new(1)
+        t.fill_(float(use_p2p))
+        comm.allreduce(t, "min")
+        use_p2p = bool(float(t.cpu().item()) > 0.5)
+    if use_p2p:
+        # [pencil, return, s_x, s_y, s_z, w] (plane 0) of every rank
+        table = comm.share_pointers(ops, [ops.xbuf(0), ops.xbuf(1), ops.plane_ptr(0, 0), ops.plane_ptr(1, 0),
+                                          ops.plane_ptr(2, 0), ops.plane_ptr(4, 0)])
+        ops.set_peers([t[0] for t in table], [t[1] for t in table])
+        pbytes = nx * ny * 8
+        slot = {0: 2, 1: 3, 2: 4, 4: 5}
+
+        def put_halos(whiches):
+            for which in whiches:
+                if comm.rank > 0:  # my first plane -> the lower neighbour's upper halo (plane nzl)
+                    ops.put_plane(which, 0, table[comm.rank - 1][slot[which]] + nzl * pbytes)
+                if comm.rank < comm.size - 1:  # my last plane -> the upper neighbour's lower halo (plane -1)
+                    ops.put_plane(which, nzl - 1, table[comm.rank + 1][slot[which]] - pbytes)
+            comm.barrier()
+
+        put_halos((2,) if iso else (0, 1, 2))
+    else:
+        for which in ((2,) if iso else (0, 1, 2)):
+            _exchange_planes(ops, comm, which, nzl)
     ops.run(SLAB_FACES)
     st = ops.stats()
     lo, hi = st[0::2].clone(), st[1::2].clone()
@@ -296,9 +404,18 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
     # on the fused path the forward transform writes its spectrum straight
     # into the all-to-all send buffer and the inverse reads it back from there
     # (pack / unpack fused into the transforms)
-    spec = send if fused else None
+    spec = None if use_p2p else (send if fused else None)
 
     def zsolve_and_back(first):
+        if use_p2p:
+            # the forward stage stored the spectrum into the peers' pencil
+            # buffers; the scalar all-reduce after it was the barrier
+            ops.run(SLAB_ZSOLVE, 0, None)  # own pencil buffer -> the owners' return buffers
+            comm.allreduce(xbuf[4:5])      # ... and the barrier before the inverse reads them
+            ops.run(SLAB_FINALIZE, FIN_THOMAS)
+            ops.run(SLAB_INVERSE, 1 if first else 2, None)
+            put_halos((4,))
+            return
         if not fused:
             ops.run(SLAB_PACK, 0, send)
         comm.alltoall(recv, send)
@@ -344,7 +461,7 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
 
 
 def virtual_slab_solve(field_cube, grid, nranks: int, p_in=1.0, p_out=0.0, rtol=1e-9, ref_mode="opt",
-                       max_iter=1024, device=None) -> list:
+                       max_iter=1024, device=None, p2p=None) -> list:
     """Run the z-slab solve with `nranks` virtual ranks on one GPU (threads +
     device copies stand in for NCCL); field_cube: canonical (nzg, ny, nx)
     CUDA tensor (isotropic field).  Returns every rank's report."""
@@ -363,7 +480,7 @@ def virtual_slab_solve(field_cube, grid, nranks: int, p_in=1.0, p_out=0.0, rtol=
             k0, nzl = slab_bounds(nzg, nranks, r)
             k = field_cube[k0:k0 + nzl].contiguous().reshape(-1)
             ops = CudaSlabOps(nx, ny, nzg, k0, nzl, nranks, r, lx, ly, lz, dev)
-            out[r] = slab_solve(ops, comms[r], k, k, k, grid, p_in, p_out, rtol, ref_mode, max_iter)
+            out[r] = slab_solve(ops, comms[r], k, k, k, grid, p_in, p_out, rtol, ref_mode, max_iter, p2p=p2p)
         except BaseException as exc:  # surface worker failures
             errs.append(exc)
             comms[r].hub.barrier.abort()

@@ -335,6 +335,14 @@ def run_b200(args, rank, world, local_rank):
         "iteration_frac": round(sum(kern[k]["bytes_per_launch"] * kern[k]["launches"] for k in it_kernels) / 1e9
                                 / (sum(kern[k]["ms_total"] for k in it_kernels) * 1e-3) / peaks["hbm_gbs"], 4),
     }
+    if "stencil" in kern:
+        # SURVEY 8(d)'s accounting: 160 B/cell per iteration for the minimal
+        # unfused pass structure; the fused kernels move 89, so this effective
+        # fraction is what the iteration achieves against that budget
+        its = kern["stencil"]["launches"]
+        roofline["survey_bytes_per_cell"] = 160
+        roofline["survey_effective_frac"] = round(160 * N * its / 1e9 / (sum(kern[k]["ms_total"] for k in it_kernels)
+                                                                        * 1e-3) / peaks["hbm_gbs"], 4)
 
     # end-to-end through the public API with host buffers
     e2e = None

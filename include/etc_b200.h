@@ -117,6 +117,14 @@ int etc_keep_solution(etc_plan* plan, int keep);
  * (SciPy SuperLU sweeps) is out of scope and has no kind. */
 int etc_set_precond(etc_plan* plan, int kind);
 
+/* Arithmetic precision of the following etc_coefficient_stats / etc_solve
+ * calls (homogenize's precision="f64" | "f32", pipeline.py:147-160): 64
+ * (default) or 32.  At 32 the field is cast to float32 and the faces,
+ * operator, transforms, z elimination and PCG vectors are float32, as the
+ * reference does with dtype float32; the statistics then come from the
+ * float32 faces.  Single-GPU plans; fct and none preconditioners. */
+int etc_set_precision(etc_plan* plan, int bits);
+
 /* Copy the solution vector p of the last solve (canonical layout); requires
  * etc_keep_solution(plan, 1) before the solve. */
 int etc_get_solution(etc_plan* plan, double* dst, int dst_on_device);

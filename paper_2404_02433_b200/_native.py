@@ -21,7 +21,7 @@ EXPORTS = (
     "etc_last_error", "etc_version", "etc_plan_create", "etc_plan_destroy",
     "etc_plan_device_bytes", "etc_load_field", "etc_select_axis",
     "etc_coefficient_stats", "etc_set_reference", "etc_solve", "etc_keep_solution",
-    "etc_set_precond", "etc_get_solution",
+    "etc_set_precond", "etc_set_precision", "etc_get_solution",
     "etc_apply_operator", "etc_dct2_xy", "etc_dct3_xy", "etc_thomas",
     "etc_apply_precond", "etc_build_rhs", "etc_profile", "etc_profile_read",
     "etc_voxelize_balls", "etc_voxelize_fibres", "etc_fill_channels", "etc_slab_create", "etc_slab_load", "etc_slab_plane",
@@ -70,6 +70,7 @@ _SIGS = {
     "etc_solve": (_I, [_P, _D, _D, _D, _I, C.POINTER(SolveInfo), _DP]),
     "etc_keep_solution": (_I, [_P, _I]),
     "etc_set_precond": (_I, [_P, _I]),
+    "etc_set_precision": (_I, [_P, _I]),
     "etc_get_solution": (_I, [_P, _P, _I]),
     "etc_apply_operator": (_I, [_P, _P, _P]),
     "etc_dct2_xy": (_I, [_P, _P, _P]),

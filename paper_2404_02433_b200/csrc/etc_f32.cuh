@@ -1,0 +1,621 @@
+// etc_f32.cuh — the single-precision path (homogenize(..., precision="f32"),
+// /root/reference/pkg/src/etchomo/pipeline.py:147-160).  Included at the end of
+// etc_b200.cu; selected per plan with etc_set_precision(plan, 32).
+//
+// What the reference does in f32 (and this file mirrors, op by op):
+//   * the field is cast to float32 (pipeline.py:155), s = k / float32(h)**2
+//     (tpfa.py:19-26), faces ((2a)b)/(a+b) and the Dirichlet layers 2 s_z in
+//     float32 (tpfa.py:29-30, 102-107);
+//   * apply_operator in float32 with the numpy association order
+//     (tpfa.py:117-130);
+//   * the FCT preconditioner: complex64 transforms (transforms.py:83-133),
+//     plane shifts and z_diag computed in float64 then cast to float32, the
+//     elimination in float32 (preconditioner.py:178-250);
+//   * PCG vectors in float32; np.dot / np.linalg.norm return float32 values;
+//     the scalars alpha, beta are Python floats cast back to float32 where they
+//     scale a vector (krylov.py:56-90), eps = finfo(float32).eps.
+// Dots are accumulated here in float64 and rounded to float32 (numpy's sdot
+// accumulates in float32; the difference is float32 rounding, which the f32
+// parity tolerance covers).
+//
+// Kernels are one-pass and simple: f32 halves the bytes of every vector, and
+// this path is the reference's precision study, not the benchmark.  The 2-D
+// transforms run as two line passes (x-lines, then y-lines / the reverse for
+// the inverse), each a batch of pair-packed complex lines in shared memory
+// (radix-2 FFT for power-of-two lengths, direct DFT otherwise); the z-solve
+// is the reference's Thomas elimination, one thread per mode column, with the
+// elimination coefficients in a scratch vector.
+
+__device__ __forceinline__ float harm32(float a, float b) {
+  return __fdiv_rn(__fmul_rn(__fmul_rn(2.0f, a), b), __fadd_rn(a, b));
+}
+
+__device__ __forceinline__ double f32r(double v) { return (double)(float)v; }  // np.float32 result of a dot
+__device__ __forceinline__ double f32norm(double rr) { return (double)sqrtf((float)rr); }
+
+__device__ __forceinline__ void fin_stencil32(Ctl* ctl, double qw, double qq, double ww) {
+  const double eps = 1.1920928955078125e-07;  // finfo(float32).eps
+  qw = f32r(qw);
+  ctl->last_qw = qw;
+  if (qw <= 100.0 * eps * f32norm(qq) * f32norm(ww)) {  // krylov.py:72-75
+    ctl->status = 1;
+    ctl->bd_kind = BD_OPERATOR;
+    ctl->bd_iter = ctl->it + 1;
+    ctl->done = 1;
+  }
+  ctl->alpha = ctl->rho / qw;
+}
+
+__device__ __forceinline__ void fin_normb32(Ctl* ctl, double rr, double* hist) {
+  ctl->last_rr = rr;
+  ctl->norm_b = f32norm(rr);
+  if (ctl->norm_b == 0.0) {
+    hist[0] = 0.0;
+    ctl->converged = 1;
+    ctl->done = 1;
+  } else {
+    hist[0] = 1.0;
+  }
+}
+
+__device__ __forceinline__ void fin_update32(Ctl* ctl, double rr, double* hist) {
+  ctl->last_rr = rr;
+  const double rel = f32norm(rr) / ctl->norm_b;
+  if (!isfinite(rel)) {
+    ctl->status = 1;
+    ctl->bd_kind = BD_NONFINITE;
+    ctl->bd_iter = ctl->it + 1;
+    ctl->done = 1;
+    return;
+  }
+  ctl->it += 1;
+  hist[ctl->it] = rel;
+  if (rel <= ctl->rtol) {
+    ctl->converged = 1;
+    ctl->done = 1;
+  }
+}
+
+// canonical cell c = (k*ny + j)*nx + i
+struct Cell3 {
+  int i, j, k;
+};
+__device__ __forceinline__ Cell3 cell3(const Geom& g, long long c) {
+  Cell3 r;
+  r.k = (int)(c / g.plane);
+  const long long rem = c - (long long)r.k * g.plane;
+  r.j = (int)(rem / g.nx);
+  r.i = (int)(rem - (long long)r.j * g.nx);
+  return r;
+}
+
+// faces along canonical axis a from the permuted conductivity kap (float64 as
+// loaded): s = float32(k) / h2f, face between c and its + neighbour; on the
+// z pass also t_in, t_out = 2 s_z on the two Dirichlet layers
+__global__ void k32_faces(Geom g, int a, const double* __restrict__ kap, float h2f, float* __restrict__ face,
+                          float* __restrict__ tb) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long step = a == 0 ? 1 : (a == 1 ? (long long)g.nx : g.plane);
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    const Cell3 p = cell3(g, c);
+    const float s = __fdiv_rn((float)kap[c], h2f);
+    const bool has = a == 0 ? p.i + 1 < g.nx : (a == 1 ? p.j + 1 < g.ny : p.k + 1 < g.nz);
+    face[c] = has ? harm32(s, __fdiv_rn((float)kap[c + step], h2f)) : 0.0f;
+    if (a == 2) {
+      const long long col = c - (long long)p.k * g.plane;
+      if (p.k == 0) tb[col] = __fmul_rn(2.0f, s);
+      if (p.k == g.nz - 1) tb[g.plane + col] = __fmul_rn(2.0f, s);
+    }
+  }
+}
+
+// exact min/max of tx, ty, tz, t_in/2, t_out/2 (preconditioner.py:94-108);
+// positive floats order like their bit patterns
+__global__ void k32_stats(Geom g, const float* __restrict__ tx, const float* __restrict__ ty,
+                          const float* __restrict__ tz, const float* __restrict__ tb, unsigned* __restrict__ mm) {
+  unsigned lo[5], hi[5];
+#pragma unroll
+  for (int a = 0; a < 5; ++a) { lo[a] = 0x7f800000u; hi[a] = 0u; }
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    const Cell3 p = cell3(g, c);
+    if (p.i + 1 < g.nx) { const unsigned v = __float_as_uint(tx[c]); lo[0] = min(lo[0], v); hi[0] = max(hi[0], v); }
+    if (p.j + 1 < g.ny) { const unsigned v = __float_as_uint(ty[c]); lo[1] = min(lo[1], v); hi[1] = max(hi[1], v); }
+    if (p.k + 1 < g.nz) { const unsigned v = __float_as_uint(tz[c]); lo[2] = min(lo[2], v); hi[2] = max(hi[2], v); }
+    if (c < g.plane) {
+      const unsigned vi = __float_as_uint(__fdiv_rn(tb[c], 2.0f));
+      const unsigned vo = __float_as_uint(__fdiv_rn(tb[g.plane + c], 2.0f));
+      lo[3] = min(lo[3], vi); hi[3] = max(hi[3], vi);
+      lo[4] = min(lo[4], vo); hi[4] = max(hi[4], vo);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 5; ++a) {
+    const unsigned l = __reduce_min_sync(0xffffffffu, lo[a]), h = __reduce_max_sync(0xffffffffu, hi[a]);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(mm + 2 * a, l);
+      atomicMax(mm + 2 * a + 1, h);
+    }
+  }
+}
+
+// b = t_in p_in on k = 0, += t_out p_out on k = nz-1 (tpfa.py:150-167); r = b,
+// p = 0, ||b|| (krylov.py:57-68)
+__global__ void k32_rhs(Geom g, const float* __restrict__ tb, float pin, float pout, float* __restrict__ r,
+                        float* __restrict__ p, Ctl* ctl, double* partials, unsigned* counter, double* hist) {
+  double rr = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    const long long k = c / g.plane, col = c - k * g.plane;
+    float b = 0.0f;
+    if (k == 0) b = __fmul_rn(tb[col], pin);
+    if (k == g.nz - 1) b = __fadd_rn(b, __fmul_rn(tb[g.plane + col], pout));
+    r[c] = b;
+    p[c] = 0.0f;
+    rr = fma((double)b, (double)b, rr);
+  }
+  double v[1] = {rr};
+  grid_sum_finalize<1>(v, partials, counter, [&](double (&t)[1]) { fin_normb32(ctl, t[0], hist); });
+}
+
+// w = z + float32(beta) w_old (w = z on the first iteration), q = A w in the
+// association order of tpfa.py:117-130, dots q.w, q.q, w.w -> alpha
+template <bool FIRST>
+__global__ void k32_stencil(Geom g, const float* __restrict__ tx, const float* __restrict__ ty,
+                            const float* __restrict__ tz, const float* __restrict__ tb, const float* __restrict__ z,
+                            const float* __restrict__ wold, float* __restrict__ wnew, float* __restrict__ q, Ctl* ctl,
+                            double* partials, unsigned* counter, int pcg) {
+  if (pcg && ctl->done) return;
+  const float bf = FIRST ? 0.0f : (float)ctl->beta;
+  auto W = [&](long long idx) -> float { return FIRST ? z[idx] : __fadd_rn(z[idx], __fmul_rn(bf, wold[idx])); };
+  double dqw = 0.0, dqq = 0.0, dww = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < g.n; c += stride) {
+    const Cell3 p = cell3(g, c);
+    const float u = W(c);
+    float acc = 0.0f;
+    if (p.i > 0) acc = __fadd_rn(acc, __fmul_rn(tx[c - 1], __fsub_rn(u, W(c - 1))));
+    if (p.i + 1 < g.nx) acc = __fsub_rn(acc, __fmul_rn(tx[c], __fsub_rn(W(c + 1), u)));
+    if (p.j > 0) acc = __fadd_rn(acc, __fmul_rn(ty[c - g.nx], __fsub_rn(u, W(c - g.nx))));
+    if (p.j + 1 < g.ny) acc = __fsub_rn(acc, __fmul_rn(ty[c], __fsub_rn(W(c + g.nx), u)));
+    if (p.k > 0) acc = __fadd_rn(acc, __fmul_rn(tz[c - g.plane], __fsub_rn(u, W(c - g.plane))));
+    if (p.k + 1 < g.nz) acc = __fsub_rn(acc, __fmul_rn(tz[c], __fsub_rn(W(c + g.plane), u)));
+    const long long col = c - (long long)p.k * g.plane;
+    if (p.k == 0) acc = __fadd_rn(acc, __fmul_rn(tb[col], u));
+    if (p.k == g.nz - 1) acc = __fadd_rn(acc, __fmul_rn(tb[g.plane + col], u));
+    if (wnew) wnew[c] = u;
+    q[c] = acc;
+    dqw = fma((double)acc, (double)u, dqw);
+    dqq = fma((double)acc, (double)acc, dqq);
+    dww = fma((double)u, (double)u, dww);
+  }
+  if (!pcg) return;
+  double v[3] = {dqw, dqq, dww};
+  grid_sum_finalize<3>(v, partials, counter, [&](double (&t)[3]) { fin_stencil32(ctl, t[0], t[1], t[2]); });
+}
+
+// p += float32(alpha) w, r -= float32(alpha) q, ||r|| (krylov.py:76-84)
+__global__ void k32_update(long long n, float* __restrict__ p, float* __restrict__ r, const float* __restrict__ w,
+                           const float* __restrict__ q, Ctl* ctl, double* partials, unsigned* counter, double* hist) {
+  if (ctl->done) return;
+  const float af = (float)ctl->alpha;
+  double rr = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += stride) {
+    p[c] = __fadd_rn(p[c], __fmul_rn(af, w[c]));
+    const float v = __fsub_rn(r[c], __fmul_rn(af, q[c]));
+    r[c] = v;
+    rr = fma((double)v, (double)v, rr);
+  }
+  double v[1] = {rr};
+  grid_sum_finalize<1>(v, partials, counter, [&](double (&t)[1]) { fin_update32(ctl, t[0], hist); });
+}
+
+// rho = r.z (krylov.py:65-67, 85-90) -> beta
+__global__ void k32_rz(long long n, const float* __restrict__ r, const float* __restrict__ z, Ctl* ctl,
+                       double* partials, unsigned* counter) {
+  if (ctl->done) return;
+  double s = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += stride)
+    s = fma((double)r[c], (double)z[c], s);
+  double v[1] = {s};
+  grid_sum_finalize<1>(v, partials, counter, [&](double (&t)[1]) { fin_thomas(ctl, f32r(t[0])); });
+}
+
+__device__ __forceinline__ float2 c32mul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// One pass of 1-D transforms over the lines of every z-plane along axis AX
+// (0: rows along x, 1: columns along y).  A CTA takes 2*LP neighbouring real
+// lines of one plane, packed two per complex line.  INV = 0: DCT-II
+// (transforms.py:83-104 per axis); INV = 1: the scaled DCT-III
+// (transforms.py:108-133 per axis).  tw[m] = exp(-2 pi i m/N) (m < N),
+// E[k] = (cos, sin)(pi k/2N): the tables of the float64 path, cast.
+template <int AX, int INV>
+__global__ void __launch_bounds__(256) k32_lines(Geom g, const float* src, float* dst, const float2* __restrict__ tw,
+                                                 const float2* __restrict__ E, int LP, const Ctl* ctl, int pcg) {
+  if (pcg && ctl->done) return;
+  extern __shared__ float2 sm32[];
+  const int N = AX == 0 ? g.nx : g.ny;         // line length
+  const int nl = AX == 0 ? g.ny : g.nx;        // lines per plane
+  const long long es = AX == 0 ? 1 : g.nx;     // element stride along a line
+  const long long ls = AX == 0 ? g.nx : 1;     // stride between neighbouring lines
+  const bool pow2 = (N & (N - 1)) == 0;
+  int lg = 0;
+  while ((1 << lg) < N) ++lg;
+  float2* A = sm32;
+  float2* B = sm32 + (size_t)LP * N;
+  const int groups = (nl + 2 * LP - 1) / (2 * LP);
+  const long long work = (long long)g.nz * groups;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nel = 2 * LP * N;
+  for (long long wk = blockIdx.x; wk < work; wk += gridDim.x) {
+    const long long kz = wk / groups;
+    const int l0 = (int)(wk - kz * groups) * 2 * LP;
+    const int nlines = min(2 * LP, nl - l0);
+    const long long base = kz * g.plane + (long long)l0 * ls;
+    // ---- load (coalesced: x-lines walk i fastest, y-lines walk the 2LP columns fastest)
+    for (int e = tid; e < nel; e += nt) {
+      int l, m;
+      if (AX == 0) { l = e / N; m = e - l * N; } else { m = e / (2 * LP); l = e - m * (2 * LP); }
+      const float v = l < nlines ? src[base + (long long)l * ls + (long long)m * es] : 0.0f;
+      if (!INV) {
+        int pos = makhoul_pos(m, N);
+        if (pow2 && lg) pos = (int)(__brev((unsigned)pos) >> (32 - lg));
+        reinterpret_cast<float*>(&A[(l >> 1) * N + pos])[l & 1] = v;
+      } else {
+        reinterpret_cast<float*>(&B[(l >> 1) * N + m])[l & 1] = v;
+      }
+    }
+    __syncthreads();
+    if (INV) {  // DCT-III pre-twiddle of both packed lines: Z = V1 + i V2 (dct3_pre)
+      for (int e = tid; e < LP * N; e += nt) {
+        const int f = e / N, kk = e - f * N;
+        const float2 a = B[f * N + kk];
+        const float2 b = kk ? B[f * N + N - kk] : make_float2(0.0f, 0.0f);
+        const float2 Ek = E[kk];
+        const float v1r = Ek.x * a.x + Ek.y * b.x, v1i = Ek.y * a.x - Ek.x * b.x;
+        const float v2r = Ek.x * a.y + Ek.y * b.y, v2i = Ek.y * a.y - Ek.x * b.y;
+        const int pos = pow2 && lg ? (int)(__brev((unsigned)kk) >> (32 - lg)) : kk;
+        A[f * N + pos] = make_float2(v1r - v2i, v1i + v2r);
+      }
+      __syncthreads();
+    }
+    // tw is exp(-2 pi i m/N); the inverse uses its conjugate
+    float2* Z = A;
+    if (pow2) {  // in-place radix-2 decimation in time on bit-reversed input
+      for (int h = 1; h < N; h <<= 1) {
+        const int tstep = N / (2 * h);
+        for (int e = tid; e < LP * (N / 2); e += nt) {
+          const int f = e / (N / 2), bb = e - f * (N / 2);
+          const int grp = bb / h, pos = bb - grp * h;
+          const int i0 = f * N + grp * 2 * h + pos, i1 = i0 + h;
+          float2 w = tw[pos * tstep];
+          if (INV) w.y = -w.y;  // forward: w; inverse: conj(w)
+          const float2 t = c32mul(A[i1], w);
+          const float2 a = A[i0];
+          A[i0] = make_float2(a.x + t.x, a.y + t.y);
+          A[i1] = make_float2(a.x - t.x, a.y - t.y);
+        }
+        __syncthreads();
+      }
+    } else {  // direct DFT (non-power-of-two lengths)
+      for (int e = tid; e < LP * N; e += nt) {
+        const int f = e / N, kk = e - f * N;
+        float2 acc = make_float2(0.0f, 0.0f);
+        for (int m = 0; m < N; ++m) {
+          float2 w = tw[(int)(((long long)m * kk) % N)];
+          if (INV) w.y = -w.y;
+          const float2 t = c32mul(A[f * N + m], w);
+          acc.x += t.x;
+          acc.y += t.y;
+        }
+        B[f * N + kk] = acc;
+      }
+      __syncthreads();
+      Z = B;
+    }
+    // ---- store
+    for (int e = tid; e < nel; e += nt) {
+      int l, m;
+      if (AX == 0) { l = e / N; m = e - l * N; } else { m = e / (2 * LP); l = e - m * (2 * LP); }
+      if (l >= nlines) continue;
+      float v;
+      if (!INV) {  // DCT-II recombination of the packed spectra (dct2_out)
+        const float2 a = Z[(l >> 1) * N + m];
+        const float2 b = Z[(l >> 1) * N + (m ? N - m : 0)];
+        const float2 Ek = E[m];
+        v = (l & 1) ? 0.5f * (Ek.x * (a.y + b.y) - Ek.y * (a.x - b.x))
+                    : 0.5f * (Ek.x * (a.x + b.x) + Ek.y * (a.y - b.y));
+      } else {
+        const float2 zz = Z[(l >> 1) * N + makhoul_pos(m, N)];
+        v = ((l & 1) ? zz.y : zz.x) / (float)N;
+      }
+      dst[base + (long long)l * ls + (long long)m * es] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// per-mode z elimination, one thread per (j', i') column, in the order of
+// thomas_solve_batch (preconditioner.py:215-250); the shift is formed in
+// float64 like TridiagFactors.plane_shift and cast (preconditioner.py:184-189)
+__global__ void k32_thomas(Geom g, float* __restrict__ x, float* __restrict__ upper, const double* __restrict__ wx,
+                           const double* __restrict__ wy, double kxr, double kyr, float zd0, float zdi, float zdl,
+                           float off, const Ctl* ctl, int pcg) {
+  if (pcg && ctl->done) return;
+  const long long P = g.plane;
+  const int nz = g.nz;
+  for (long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x; col < P;
+       col += (long long)gridDim.x * blockDim.x) {
+    const int ip = (int)(col % g.nx), jp = (int)(col / g.nx);
+    const float shift = (float)__dadd_rn(__dmul_rn(wx[ip], kxr), __dmul_rn(wy[jp], kyr));
+    const float diag0 = __fadd_rn(zd0, shift);
+    if (nz == 1) {
+      x[col] = __fdiv_rn(x[col], diag0);
+      continue;
+    }
+    float up = __fdiv_rn(off, diag0);
+    upper[col] = up;
+    float xp = __fdiv_rn(x[col], diag0);
+    x[col] = xp;
+    for (int k = 1; k < nz; ++k) {
+      const long long c = (long long)k * P + col;
+      const float denom = __fsub_rn(__fadd_rn(k == nz - 1 ? zdl : zdi, shift), __fmul_rn(off, up));
+      if (k < nz - 1) {
+        up = __fdiv_rn(off, denom);
+        upper[c] = up;
+      }
+      xp = __fdiv_rn(__fsub_rn(x[c], __fmul_rn(off, xp)), denom);
+      x[c] = xp;
+    }
+    for (int k = nz - 2; k >= 0; --k) {
+      const long long c = (long long)k * P + col;
+      xp = __fsub_rn(x[c], __fmul_rn(upper[c], xp));
+      x[c] = xp;
+    }
+  }
+}
+
+// outflow flux t_out hz (p[nz-1] - p_out) per column in float32
+// (tpfa.py:234-251), summed in float64 (tpfa.py:254-258)
+__global__ void k32_flux(Geom g, const float* __restrict__ tb, const float* __restrict__ p, float hz, float pout,
+                         double* out, double* partials, unsigned* counter) {
+  double s = 0.0;
+  const long long off = (long long)(g.nz - 1) * g.plane;
+  for (long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x; col < g.plane;
+       col += (long long)gridDim.x * blockDim.x)
+    s += (double)__fmul_rn(__fmul_rn(tb[g.plane + col], hz), __fsub_rn(p[off + col], pout));
+  double v[1] = {s};
+  grid_sum_finalize<1>(v, partials, counter, [&](double (&t)[1]) { *out = t[0]; });
+}
+
+__global__ void k32_tabs(int n, const double2* __restrict__ src, float2* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = make_float2((float)src[i].x, (float)src[i].y);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static int f32_alloc(etc_plan* pl, float** v, size_t count) {
+  double* d = nullptr;
+  int rc = dev_alloc(pl, &d, (count + 1) / 2);
+  *v = reinterpret_cast<float*>(d);
+  return rc;
+}
+
+static int f32_buffers(etc_plan* pl) {
+  if (pl->v32[0]) return ETC_OK;
+  const size_t n = (size_t)pl->n;
+  int rc;
+  for (int b = 0; b < 10; ++b)  // tx ty tz | p r q z w0 w1 | (unused)
+    if (b < 9 && (rc = f32_alloc(pl, &pl->v32[b], n))) return rc;
+  if ((rc = f32_alloc(pl, &pl->tb32, 2 * (size_t)pl->nx * pl->ny))) return rc;
+  if ((rc = f32_alloc(pl, reinterpret_cast<float**>(&pl->ctab32), 8 * (size_t)pl->maxd))) return rc;
+  return ETC_OK;
+}
+
+// float32 faces of the current direction from the loaded field
+static int f32_faces(etc_plan* pl) {
+  if (pl->slab) return fail(ETC_CONFIG, "precision f32 runs on single-GPU plans");
+  int rc;
+  if ((rc = f32_buffers(pl))) return rc;
+  int comp[3] = {0, 1, 2};
+  if (pl->axis == 0) { comp[0] = 2; comp[1] = 1; comp[2] = 0; }
+  if (pl->axis == 1) { comp[0] = 0; comp[1] = 2; comp[2] = 1; }
+  const double h[3] = {pl->lx / pl->nx, pl->ly / pl->ny, pl->lz / pl->nz};
+  const Geom g = geom(pl);
+  for (int a = 0; a < 3; ++a) {
+    // the permuted conductivity (scale 1) into the f64 scratch z, then faces
+    if ((rc = scale_into(pl, pl->raw[comp[a]], 1.0, pl->z))) return rc;
+    const float hf = (float)h[a];
+    const float h2f = hf * hf;  // dtype(h)**2 in float32 (tpfa.py:23-25)
+    Tm tm(pl, 6);
+    k32_faces<<<grid1d(pl, pl->n), 256, 0, pl->stream>>>(g, a, pl->z, h2f, pl->v32[a], pl->tb32);
+    CK(cudaGetLastError());
+  }
+  pl->faces32_ok = true;
+  return ETC_OK;
+}
+
+static int f32_stats(etc_plan* pl, double out[10]) {
+  int rc;
+  if (!pl->faces32_ok && (rc = f32_faces(pl))) return rc;
+  unsigned init[10];
+  for (int a = 0; a < 5; ++a) { init[2 * a] = 0x7f800000u; init[2 * a + 1] = 0u; }
+  unsigned* mm = reinterpret_cast<unsigned*>(pl->scal);
+  CK(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, pl->stream));
+  {
+    Tm tm(pl, 6);
+    k32_stats<<<grid1d(pl, pl->n), 256, 0, pl->stream>>>(geom(pl), pl->v32[0], pl->v32[1], pl->v32[2], pl->tb32, mm);
+    CK(cudaGetLastError());
+  }
+  unsigned res[10];
+  CK(cudaMemcpyAsync(res, mm, sizeof(res), cudaMemcpyDeviceToHost, pl->stream));
+  CK(cudaStreamSynchronize(pl->stream));
+  for (int i = 0; i < 10; ++i) {
+    float f;
+    std::memcpy(&f, &res[i], sizeof(f));
+    out[i] = (double)f;
+  }
+  if (pl->nx < 2) { out[0] = 1.0; out[1] = 1.0; }
+  if (pl->ny < 2) { out[2] = 1.0; out[3] = 1.0; }
+  if (pl->nz < 2) { out[4] = 1.0; out[5] = 1.0; }
+  return ETC_OK;
+}
+
+// line batch size: about 4096 packed complex elements (32 KB) per pass
+static int f32_lp(int N) { return std::max(1, std::min(32, 4096 / std::max(1, N))); }
+
+template <int AX, int INV>
+static int f32_pass(etc_plan* pl, const float* src, float* dst, int pcg) {
+  const Geom g = geom(pl);
+  const int N = AX == 0 ? pl->nx : pl->ny, nl = AX == 0 ? pl->ny : pl->nx;
+  const int LP = f32_lp(N);
+  const size_t smem = 2 * (size_t)LP * N * sizeof(float2);
+  auto kern = k32_lines<AX, INV>;
+  int rc;
+  if (smem > 48 * 1024 && (rc = prep_smem(kern, smem))) return rc;
+  const long long work = (long long)pl->nz * ((nl + 2 * LP - 1) / (2 * LP));
+  const int grid = (int)std::min<long long>(work, (long long)pl->sms * 8);
+  const float2* T = pl->ctab32;
+  const int M = pl->maxd;
+  const float2* tw = AX == 0 ? T : T + M;
+  const float2* E = AX == 0 ? T + 2 * M : T + 3 * M;
+  Tm tm(pl, INV ? 5 : 2);
+  kern<<<grid, 256, smem, pl->stream>>>(g, src, dst, tw, E, LP, pl->ctl, pcg);
+  CK(cudaGetLastError());
+  return ETC_OK;
+}
+
+// z = M^-1 r: forward 2-D DCT of r into t, the z elimination (its
+// coefficients in the scratch z), inverse 2-D DCT of t into z
+static int f32_precond(etc_plan* pl, const float* r, float* t, float* z, int pcg) {
+  int rc;
+  if ((rc = f32_pass<0, 0>(pl, r, t, pcg))) return rc;
+  if ((rc = f32_pass<1, 0>(pl, t, t, pcg))) return rc;
+  {
+    const Geom g = geom(pl);
+    const int M = pl->maxd;
+    Tm tm(pl, 3);
+    k32_thomas<<<grid1d(pl, g.plane, 128), 128, 0, pl->stream>>>(
+        g, t, z, pl->tabs, pl->tabs + M, pl->refs[0], pl->refs[1], (float)pl->zd3[0], (float)pl->zd3[1],
+        (float)pl->zd3[2], (float)(-pl->refs[2]), pl->ctl, pcg);
+    CK(cudaGetLastError());
+  }
+  if ((rc = f32_pass<1, 1>(pl, t, z, pcg))) return rc;
+  return f32_pass<0, 1>(pl, z, z, pcg);
+}
+
+static int f32_set_reference(etc_plan* pl) {
+  int rc;
+  if ((rc = f32_buffers(pl))) return rc;
+  const int n = 4 * pl->maxd;
+  k32_tabs<<<(n + 255) / 256, 256, 0, pl->stream>>>(n, pl->ctab, pl->ctab32);
+  CK(cudaGetLastError());
+  return ETC_OK;
+}
+
+static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max_iter, etc_solve_info* info,
+                   double* hist_host) {
+  int rc;
+  if (pl->precond == ETC_PRECOND_JACOBI) return fail(ETC_CONFIG, "precision f32 supports the fct and none preconditioners");
+  if (!pl->faces32_ok && (rc = f32_faces(pl))) return rc;
+  if ((rc = f32_set_reference(pl))) return rc;
+  const Geom g = geom(pl);
+  float *tx = pl->v32[0], *ty = pl->v32[1], *tz = pl->v32[2];
+  float *p = pl->v32[3], *r = pl->v32[4], *q = pl->v32[5], *z = pl->v32[6];
+  float* w[2] = {pl->v32[7], pl->v32[8]};
+  const bool none = pl->precond == ETC_PRECOND_NONE;
+  Ctl c;
+  std::memset(&c, 0, sizeof(c));
+  c.rtol = rtol;
+  c.max_iter = max_iter;
+  CK(cudaMemcpyAsync(pl->ctl, &c, sizeof(c), cudaMemcpyHostToDevice, pl->stream));
+  CK(cudaMemsetAsync(pl->counters, 0, 64 * sizeof(unsigned), pl->stream));
+  CK(cudaEventRecord(pl->ev0, pl->stream));
+  const int G = grid1d(pl, pl->n);
+  {
+    Tm tm(pl, 6);
+    k32_rhs<<<G, 256, 0, pl->stream>>>(g, pl->tb32, (float)p_in, (float)p_out, r, p, pl->ctl, pl->partials,
+                                       pl->counters + 1, pl->hist);
+    CK(cudaGetLastError());
+  }
+  // iteration 0: z = M r, rho = r.z (krylov.py:63-68)
+  const float* zv = none ? r : z;
+  if (!none && (rc = f32_precond(pl, r, q, z, 1))) return rc;
+  k32_rz<<<G, 256, 0, pl->stream>>>(pl->n, r, zv, pl->ctl, pl->partials, pl->counters + 2);
+  CK(cudaGetLastError());
+  int it = 0;
+  bool done = false;
+  while (!done && it < max_iter) {
+    const int batch = std::min(pl->check_every, max_iter - it);
+    for (int b = 0; b < batch; ++b) {
+      ++it;
+      float* wn = w[it & 1];
+      const float* wo = w[(it - 1) & 1];
+      {
+        Tm tm(pl, 0);
+        if (it == 1)
+          k32_stencil<true><<<G, 256, 0, pl->stream>>>(g, tx, ty, tz, pl->tb32, zv, nullptr, wn, q, pl->ctl,
+                                                       pl->partials, pl->counters + 0, 1);
+        else
+          k32_stencil<false><<<G, 256, 0, pl->stream>>>(g, tx, ty, tz, pl->tb32, zv, wo, wn, q, pl->ctl,
+                                                        pl->partials, pl->counters + 0, 1);
+        CK(cudaGetLastError());
+      }
+      {
+        Tm tm(pl, 1);
+        k32_update<<<G, 256, 0, pl->stream>>>(pl->n, p, r, wn, q, pl->ctl, pl->partials, pl->counters + 1,
+                                              pl->hist);
+        CK(cudaGetLastError());
+      }
+      if (!none && (rc = f32_precond(pl, r, q, z, 1))) return rc;
+      k32_rz<<<G, 256, 0, pl->stream>>>(pl->n, r, zv, pl->ctl, pl->partials, pl->counters + 2);
+      CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(pl->ctl_host, pl->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    done = pl->ctl_host->done != 0;
+  }
+  CK(cudaEventRecord(pl->ev1, pl->stream));
+  CK(cudaMemcpyAsync(pl->ctl_host, pl->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pl->stream));
+  CK(cudaStreamSynchronize(pl->stream));
+  const Ctl& h = *pl->ctl_host;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, pl->ev0, pl->ev1);
+  std::memset(info, 0, sizeof(*info));
+  info->iterations = h.it;
+  info->converged = h.converged;
+  info->status = h.status ? ETC_BREAKDOWN : ETC_OK;
+  info->breakdown_iter = h.bd_iter;
+  info->breakdown_kind = h.bd_kind;
+  info->norm_b = h.norm_b;
+  info->device_ms = ms;
+  if (hist_host) CK(cudaMemcpy(hist_host, pl->hist, (size_t)(h.it + 1) * sizeof(double), cudaMemcpyDeviceToHost));
+  if (h.status) return fail(ETC_BREAKDOWN, "PCG breakdown");
+  {
+    Tm tm(pl, 6);
+    const float hzf = (float)(pl->lz / pl->nz);
+    k32_flux<<<grid1d(pl, g.plane, 256, 2), 256, 0, pl->stream>>>(g, pl->tb32, p, hzf, (float)p_out, pl->scal + 20,
+                                                                  pl->partials, pl->counters + 3);
+    CK(cudaGetLastError());
+  }
+  double fs = 0.0;
+  CK(cudaMemcpyAsync(&fs, pl->scal + 20, sizeof(double), cudaMemcpyDeviceToHost, pl->stream));
+  CK(cudaStreamSynchronize(pl->stream));
+  info->flux_sum = fs;
+  info->kappa_eff = pl->lz * fs / ((double)pl->nx * pl->ny * (p_in - p_out));
+  return ETC_OK;
+}
+
+extern "C" int etc_set_precision(etc_plan* pl, int bits) {
+  if (!pl) return fail(ETC_CONFIG, "null plan");
+  if (bits != 32 && bits != 64) return fail(ETC_CONFIG, "precision must be 32 or 64 bits");
+  if (bits == 32 && pl->slab) return fail(ETC_CONFIG, "precision f32 runs on single-GPU plans");
+  pl->prec32 = bits == 32;
+  return ETC_OK;
+}

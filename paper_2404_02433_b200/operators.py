@@ -26,6 +26,7 @@ class DeviceSystem:
         self.plan = get_plan(fld.grid, device)
         self.plan.load_field(fld, force=True)
         self.grid = self.plan.select_axis(self.boundary.axis)
+        self.plan.set_precision("f64")  # the operator-level entry points are float64
         self.stats = self.plan.coefficient_stats()
         if refs is None:
             refs = solve_reference_lp(self.stats) if ref_mode == "opt" else ones_reference(self.stats)

@@ -124,20 +124,24 @@ def z_chain_diagonal(nz: int, refs: ReferenceParams) -> np.ndarray:
     return zd
 
 
-def check_pivots(nz: int, z_diag: np.ndarray, refs: ReferenceParams) -> None:
+def check_pivots(nz: int, z_diag: np.ndarray, refs: ReferenceParams, dtype=np.float64) -> None:
     """Raise FloatingPointError exactly when the reference's non-pivoting
     elimination would (preconditioner.py:229-244).  Every plane shift is
     >= 0 (shift(0,0) = 0) and the pivots grow with the shift, so the
-    zero-shift column carries the smallest pivots; replay it on the host."""
-    off = -refs.kz_ref
-    d0 = z_diag[0] + 0.0
+    zero-shift column carries the smallest pivots; replay it on the host,
+    in the solve's dtype (z_diag and off cast as TridiagFactors does,
+    preconditioner.py:189-199)."""
+    dt = np.dtype(dtype).type
+    z_diag = np.asarray(z_diag).astype(dt)
+    off = dt(-refs.kz_ref)
+    d0 = z_diag[0] + dt(0.0)
     if d0 <= 0:
         raise FloatingPointError("non-positive pivot in tridiagonal solve")
     if nz == 1:
         return
     upper = off / d0
     for k in range(1, nz):
-        denom = (z_diag[k] + 0.0) - off * upper
+        denom = (z_diag[k] + dt(0.0)) - off * upper
         if denom <= 0:
             raise FloatingPointError(f"non-positive pivot in tridiagonal solve at layer {k}")
         upper = off / denom

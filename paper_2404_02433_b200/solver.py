@@ -107,6 +107,7 @@ class DevicePlan:
                    "etc_plan_create")
         self._field_key = None
         self._keepalive = None
+        self.precision = "f64"
         self.canonical = None
         self.axis = None
         self._fin = weakref.finalize(self, self.lib.etc_plan_destroy, self._h)
@@ -171,7 +172,7 @@ class DevicePlan:
         wx = eigen_weights(g.nx)
         wy = eigen_weights(g.ny)
         zd = z_chain_diagonal(g.nz, refs)
-        check_pivots(g.nz, zd, refs)
+        check_pivots(g.nz, zd, refs, np.float32 if self.precision == "f32" else np.float64)
         r5 = (C.c_double * 5)(*refs.constants())
         dp = _native._DP
         _check(self.lib.etc_set_reference(self._h, r5, wx.ctypes.data_as(dp), wy.ctypes.data_as(dp),
@@ -189,6 +190,11 @@ class DevicePlan:
                                     info.breakdown_iter)
         _check(rc, "etc_solve")
         return info, history
+
+    def set_precision(self, precision: str) -> None:
+        """Arithmetic of the next stats / solve: "f64" | "f32" (pipeline.py:147-160)."""
+        _check(self.lib.etc_set_precision(self._h, 32 if precision == "f32" else 64), "etc_set_precision")
+        self.precision = precision
 
     def keep_solution(self, keep: bool) -> None:
         _check(self.lib.etc_keep_solution(self._h, 1 if keep else 0), "etc_keep_solution")
@@ -294,8 +300,10 @@ def _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_
     if kind == "ssor":
         raise ConfigError("ssor (SciPy SuperLU triangular sweeps) is not implemented on the device; "
                           "use fct, jacobi or none")
-    if precision != "f64":
-        raise ConfigError("the device solver computes in f64 only")
+    if precision == "f32" and kind == "jacobi":
+        raise ConfigError("precision f32 runs with the fct and none preconditioners")
+    if precision == "f32" and keep_solution:
+        raise ConfigError("the full-solution mode runs in f64")
     if rtol <= 0.0:
         raise ValueError("rtol must be positive")
     if max_iter < 1:
@@ -308,6 +316,7 @@ def _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_
         t0 = time.perf_counter()
         plan.load_field(fld)
         plan.select_axis(boundary.axis)
+        plan.set_precision(precision)
         stats = plan.coefficient_stats()
         refs = solve_reference_lp(stats) if ref_mode == "opt" else ones_reference(stats)
         plan.set_reference(refs)

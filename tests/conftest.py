@@ -42,3 +42,10 @@ def golden_channels():
     import json
 
     return json.loads((GOLDEN / "solves_channels.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def golden_f32():
+    import json
+
+    return json.loads((GOLDEN / "solves_f32.json").read_text())

@@ -1,0 +1,48 @@
+"""Reference solves in single precision (homogenize(..., precision="f32"),
+pipeline.py:147-160: the field cast to float32, faces, operator, transforms
+(complex64 pocketfft), tridiagonal solves and PCG vectors in float32, PCG
+scalars in Python floats), the SURVEY 8(f) row-1 precision path.  Each case
+also records the float64 solve of the same problem at the same rtol, whose
+distance to the f32 result is the scale single precision can resolve.
+Imports /root/reference (build container only); writes
+tests/golden/solves_f32.json.
+
+    python tests/golden/make_golden_f32.py
+"""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, "/root/reference/pkg/src")
+import etchomo as E  # noqa: E402
+
+CASES = [
+    # kind, n, contrast, axis, rtol, precond
+    ("center-ball", 64, 10.0, "z", 1e-6, "fct"),   # 15 iterations, 1.156023888674
+    ("random-a", 32, 100.0, "x", 1e-5, "fct"),
+    ("random-a", 32, 100.0, "y", 1e-5, "fct"),
+    ("random-a", 32, 100.0, "z", 1e-5, "fct"),
+    ("random-a", 24, 10.0, "z", 1e-6, "fct"),      # non-power-of-two planes
+    ("center-ball", 20, 100.0, "x", 1e-5, "fct"),
+    ("random-a", 64, 100.0, "z", 1e-5, "fct"),
+    ("random-a", 16, 10.0, "z", 1e-4, "none"),
+]
+
+pr = E.RANDOM_BALL_PRESETS["a"]
+out = []
+for kind, n, c, ax, rtol, pc in CASES:
+    if kind == "random-a":
+        field = E.gen_random_balls(n, pr["count"], pr["r_min"], pr["r_max"], c, pr["seed"])
+    else:
+        field = E.gen_center_ball(n, c)
+    bc = E.BoundaryConfig(E.Axis(ax), 1.0, 0.0)
+    rep = E.homogenize(field, bc, rtol, precond=pc, precision="f32")
+    r64 = E.homogenize(field, bc, rtol, precond=pc, precision="f64")
+    out.append(dict(kind=kind, n=n, kappa=c, axis=ax, rtol=rtol, precond=pc, iterations=rep.iterations,
+                    converged=rep.converged, kappa_eff=rep.kappa_eff, history=rep.relative_residuals,
+                    precision=rep.precision, refs=rep.ref_params.as_dict() if rep.ref_params else None,
+                    f64_iterations=r64.iterations, f64_kappa_eff=r64.kappa_eff))
+    print(kind, n, c, ax, rtol, pc, rep.iterations, repr(rep.kappa_eff), r64.iterations, repr(r64.kappa_eff),
+          flush=True)
+path = Path(__file__).resolve().parent / "solves_f32.json"
+path.write_text(json.dumps(out, indent=1) + "\n")

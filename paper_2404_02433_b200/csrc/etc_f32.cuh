@@ -22,7 +22,7 @@
 // this path is the reference's precision study, not the benchmark.  The 2-D
 // transforms run as two line passes (x-lines, then y-lines / the reverse for
 // the inverse), each a batch of pair-packed complex lines in shared memory
-// (radix-2 FFT for power-of-two lengths, direct DFT otherwise); the z-solve
+// (radix-2 Stockham FFT for power-of-two lengths, direct DFT otherwise); the z-solve
 // is the reference's Thomas elimination, one thread per mode column, with the
 // elimination coefficients in a scratch vector.
 
@@ -161,33 +161,46 @@ __global__ void k32_rhs(Geom g, const float* __restrict__ tb, float pin, float p
 // w = z + float32(beta) w_old (w = z on the first iteration), q = A w in the
 // association order of tpfa.py:117-130, dots q.w, q.q, w.w -> alpha
 template <bool FIRST>
-__global__ void k32_stencil(Geom g, const float* __restrict__ tx, const float* __restrict__ ty,
-                            const float* __restrict__ tz, const float* __restrict__ tb, const float* __restrict__ z,
-                            const float* __restrict__ wold, float* __restrict__ wnew, float* __restrict__ q, Ctl* ctl,
-                            double* partials, unsigned* counter, int pcg) {
+__global__ void __launch_bounds__(256) k32_stencil(Geom g, int kchunk, const float* __restrict__ tx,
+                                                   const float* __restrict__ ty, const float* __restrict__ tz,
+                                                   const float* __restrict__ tb, const float* __restrict__ z,
+                                                   const float* __restrict__ wold, float* __restrict__ wnew,
+                                                   float* __restrict__ q, Ctl* ctl, double* partials,
+                                                   unsigned* counter, int pcg) {
   if (pcg && ctl->done) return;
   const float bf = FIRST ? 0.0f : (float)ctl->beta;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const long long P = g.plane;
   auto W = [&](long long idx) -> float { return FIRST ? z[idx] : __fadd_rn(z[idx], __fmul_rn(bf, wold[idx])); };
   double dqw = 0.0, dqq = 0.0, dww = 0.0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < g.n; c += stride) {
-    const Cell3 p = cell3(g, c);
-    const float u = W(c);
-    float acc = 0.0f;
-    if (p.i > 0) acc = __fadd_rn(acc, __fmul_rn(tx[c - 1], __fsub_rn(u, W(c - 1))));
-    if (p.i + 1 < g.nx) acc = __fsub_rn(acc, __fmul_rn(tx[c], __fsub_rn(W(c + 1), u)));
-    if (p.j > 0) acc = __fadd_rn(acc, __fmul_rn(ty[c - g.nx], __fsub_rn(u, W(c - g.nx))));
-    if (p.j + 1 < g.ny) acc = __fsub_rn(acc, __fmul_rn(ty[c], __fsub_rn(W(c + g.nx), u)));
-    if (p.k > 0) acc = __fadd_rn(acc, __fmul_rn(tz[c - g.plane], __fsub_rn(u, W(c - g.plane))));
-    if (p.k + 1 < g.nz) acc = __fsub_rn(acc, __fmul_rn(tz[c], __fsub_rn(W(c + g.plane), u)));
-    const long long col = c - (long long)p.k * g.plane;
-    if (p.k == 0) acc = __fadd_rn(acc, __fmul_rn(tb[col], u));
-    if (p.k == g.nz - 1) acc = __fadd_rn(acc, __fmul_rn(tb[g.plane + col], u));
-    if (wnew) wnew[c] = u;
-    q[c] = acc;
-    dqw = fma((double)acc, (double)u, dqw);
-    dqq = fma((double)acc, (double)acc, dqq);
-    dww = fma((double)u, (double)u, dww);
+  // work item = (32x8 column tile, z chunk); each thread marches its column
+  const int tx_n = (nx + 31) / 32, ty_n = (ny + 7) / 8, nch = (nz + kchunk - 1) / kchunk;
+  const long long work = (long long)tx_n * ty_n * nch;
+  for (long long wk = blockIdx.x; wk < work; wk += gridDim.x) {
+    const int ch = (int)(wk / ((long long)tx_n * ty_n));
+    const int tt = (int)(wk - (long long)ch * tx_n * ty_n);
+    const int i = (tt % tx_n) * 32 + (threadIdx.x & 31), j = (tt / tx_n) * 8 + (threadIdx.x >> 5);
+    if (i >= nx || j >= ny) continue;
+    const int k0 = ch * kchunk, k1 = min(nz, k0 + kchunk);
+    const long long col = (long long)j * nx + i;
+    for (int k = k0; k < k1; ++k) {
+      const long long c = (long long)k * P + col;
+      const float u = W(c);
+      float acc = 0.0f;
+      if (i > 0) acc = __fadd_rn(acc, __fmul_rn(tx[c - 1], __fsub_rn(u, W(c - 1))));
+      if (i + 1 < nx) acc = __fsub_rn(acc, __fmul_rn(tx[c], __fsub_rn(W(c + 1), u)));
+      if (j > 0) acc = __fadd_rn(acc, __fmul_rn(ty[c - nx], __fsub_rn(u, W(c - nx))));
+      if (j + 1 < ny) acc = __fsub_rn(acc, __fmul_rn(ty[c], __fsub_rn(W(c + nx), u)));
+      if (k > 0) acc = __fadd_rn(acc, __fmul_rn(tz[c - P], __fsub_rn(u, W(c - P))));
+      if (k + 1 < nz) acc = __fsub_rn(acc, __fmul_rn(tz[c], __fsub_rn(W(c + P), u)));
+      if (k == 0) acc = __fadd_rn(acc, __fmul_rn(tb[col], u));
+      if (k == nz - 1) acc = __fadd_rn(acc, __fmul_rn(tb[P + col], u));
+      if (wnew) wnew[c] = u;
+      q[c] = acc;
+      dqw = fma((double)acc, (double)u, dqw);
+      dqq = fma((double)acc, (double)acc, dqq);
+      dww = fma((double)u, (double)u, dww);
+    }
   }
   if (!pcg) return;
   double v[3] = {dqw, dqq, dww};
@@ -233,20 +246,24 @@ __device__ __forceinline__ float2 c32mul(float2 a, float2 b) {
 // (transforms.py:83-104 per axis); INV = 1: the scaled DCT-III
 // (transforms.py:108-133 per axis).  tw[m] = exp(-2 pi i m/N) (m < N),
 // E[k] = (cos, sin)(pi k/2N): the tables of the float64 path, cast.
-template <int AX, int INV>
+// LG > 0: N = 2^LG at compile time (index math in shifts, FFT stages
+// unrolled); LG = 0: runtime length (radix-2 if a power of two, else DFT).
+__host__ __device__ constexpr int f32_lp_of(int N) { return N >= 4096 ? 1 : (4096 / N > 32 ? 32 : 4096 / N); }
+
+template <int AX, int INV, int LG>
 __global__ void __launch_bounds__(256) k32_lines(Geom g, const float* src, float* dst, const float2* __restrict__ tw,
-                                                 const float2* __restrict__ E, int LP, const Ctl* ctl, int pcg) {
+                                                 const float2* __restrict__ E, int LPrt, const Ctl* ctl, int pcg) {
   if (pcg && ctl->done) return;
   extern __shared__ float2 sm32[];
-  const int N = AX == 0 ? g.nx : g.ny;         // line length
+  const int N = LG ? (1 << LG) : (AX == 0 ? g.nx : g.ny);  // line length
+  const int LP = LG ? f32_lp_of(1 << LG) : LPrt;
+  const int PN = N + 1;                        // padded line pitch (float2)
   const int nl = AX == 0 ? g.ny : g.nx;        // lines per plane
-  const long long es = AX == 0 ? 1 : g.nx;     // element stride along a line
-  const long long ls = AX == 0 ? g.nx : 1;     // stride between neighbouring lines
-  const bool pow2 = (N & (N - 1)) == 0;
-  int lg = 0;
-  while ((1 << lg) < N) ++lg;
+  const int es = AX == 0 ? 1 : g.nx;           // element stride along a line (in-plane: 32-bit)
+  const int ls = AX == 0 ? g.nx : 1;           // stride between neighbouring lines
+  const bool pow2 = LG ? true : (N & (N - 1)) == 0;
   float2* A = sm32;
-  float2* B = sm32 + (size_t)LP * N;
+  float2* B = sm32 + (size_t)LP * PN;
   const int groups = (nl + 2 * LP - 1) / (2 * LP);
   const long long work = (long long)g.nz * groups;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -255,52 +272,56 @@ __global__ void __launch_bounds__(256) k32_lines(Geom g, const float* src, float
     const long long kz = wk / groups;
     const int l0 = (int)(wk - kz * groups) * 2 * LP;
     const int nlines = min(2 * LP, nl - l0);
-    const long long base = kz * g.plane + (long long)l0 * ls;
+    const float* sp = src + kz * g.plane + l0 * ls;
+    float* dp = dst + kz * g.plane + l0 * ls;
     // ---- load (coalesced: x-lines walk i fastest, y-lines walk the 2LP columns fastest)
     for (int e = tid; e < nel; e += nt) {
       int l, m;
       if (AX == 0) { l = e / N; m = e - l * N; } else { m = e / (2 * LP); l = e - m * (2 * LP); }
-      const float v = l < nlines ? src[base + (long long)l * ls + (long long)m * es] : 0.0f;
-      if (!INV) {
-        int pos = makhoul_pos(m, N);
-        if (pow2 && lg) pos = (int)(__brev((unsigned)pos) >> (32 - lg));
-        reinterpret_cast<float*>(&A[(l >> 1) * N + pos])[l & 1] = v;
-      } else {
-        reinterpret_cast<float*>(&B[(l >> 1) * N + m])[l & 1] = v;
-      }
+      const float v = l < nlines ? sp[l * ls + m * es] : 0.0f;
+      if (!INV)  // Makhoul gather: evens ascending, odds descending (transforms.py:41-43)
+        reinterpret_cast<float*>(&A[(l >> 1) * PN + makhoul_pos(m, N)])[l & 1] = v;
+      else
+        reinterpret_cast<float*>(&B[(l >> 1) * PN + m])[l & 1] = v;
     }
     __syncthreads();
     if (INV) {  // DCT-III pre-twiddle of both packed lines: Z = V1 + i V2 (dct3_pre)
       for (int e = tid; e < LP * N; e += nt) {
         const int f = e / N, kk = e - f * N;
-        const float2 a = B[f * N + kk];
-        const float2 b = kk ? B[f * N + N - kk] : make_float2(0.0f, 0.0f);
+        const float2 a = B[f * PN + kk];
+        const float2 b = kk ? B[f * PN + N - kk] : make_float2(0.0f, 0.0f);
         const float2 Ek = E[kk];
         const float v1r = Ek.x * a.x + Ek.y * b.x, v1i = Ek.y * a.x - Ek.x * b.x;
         const float v2r = Ek.x * a.y + Ek.y * b.y, v2i = Ek.y * a.y - Ek.x * b.y;
-        const int pos = pow2 && lg ? (int)(__brev((unsigned)kk) >> (32 - lg)) : kk;
-        A[f * N + pos] = make_float2(v1r - v2i, v1i + v2r);
+        A[f * PN + kk] = make_float2(v1r - v2i, v1i + v2r);
       }
       __syncthreads();
     }
-    // tw is exp(-2 pi i m/N); the inverse uses its conjugate
+    // ---- FFT of the LP packed lines in A (natural order in and out);
+    // tw is exp(-2 pi i m/N), the inverse uses its conjugate
     float2* Z = A;
-    if (pow2) {  // in-place radix-2 decimation in time on bit-reversed input
-      for (int h = 1; h < N; h <<= 1) {
-        const int tstep = N / (2 * h);
+    if (pow2) {  // radix-2 Stockham auto-sort, ping-pong A <-> B
+      float2 *x = A, *y = B;
+#pragma unroll
+      for (int st = 0; st < (LG ? LG : 31); ++st) {
+        const int Ns = 1 << st;
+        if (!LG && Ns >= N) break;
+        const int tstep = N / (2 * Ns);
         for (int e = tid; e < LP * (N / 2); e += nt) {
-          const int f = e / (N / 2), bb = e - f * (N / 2);
-          const int grp = bb / h, pos = bb - grp * h;
-          const int i0 = f * N + grp * 2 * h + pos, i1 = i0 + h;
-          float2 w = tw[pos * tstep];
-          if (INV) w.y = -w.y;  // forward: w; inverse: conj(w)
-          const float2 t = c32mul(A[i1], w);
-          const float2 a = A[i0];
-          A[i0] = make_float2(a.x + t.x, a.y + t.y);
-          A[i1] = make_float2(a.x - t.x, a.y - t.y);
+          const int f = e / (N / 2), j = e - f * (N / 2);
+          const int k = j & (Ns - 1);
+          float2 w = tw[k * tstep];
+          if (INV) w.y = -w.y;
+          const float2 a = x[f * PN + j];
+          const float2 t = c32mul(x[f * PN + j + N / 2], w);
+          const int d = f * PN + ((j - k) << 1) + k;
+          y[d] = make_float2(a.x + t.x, a.y + t.y);
+          y[d + Ns] = make_float2(a.x - t.x, a.y - t.y);
         }
         __syncthreads();
+        float2* tmp = x; x = y; y = tmp;
       }
+      Z = x;
     } else {  // direct DFT (non-power-of-two lengths)
       for (int e = tid; e < LP * N; e += nt) {
         const int f = e / N, kk = e - f * N;
@@ -308,11 +329,11 @@ __global__ void __launch_bounds__(256) k32_lines(Geom g, const float* src, float
         for (int m = 0; m < N; ++m) {
           float2 w = tw[(int)(((long long)m * kk) % N)];
           if (INV) w.y = -w.y;
-          const float2 t = c32mul(A[f * N + m], w);
+          const float2 t = c32mul(A[f * PN + m], w);
           acc.x += t.x;
           acc.y += t.y;
         }
-        B[f * N + kk] = acc;
+        B[f * PN + kk] = acc;
       }
       __syncthreads();
       Z = B;
@@ -324,16 +345,16 @@ __global__ void __launch_bounds__(256) k32_lines(Geom g, const float* src, float
       if (l >= nlines) continue;
       float v;
       if (!INV) {  // DCT-II recombination of the packed spectra (dct2_out)
-        const float2 a = Z[(l >> 1) * N + m];
-        const float2 b = Z[(l >> 1) * N + (m ? N - m : 0)];
+        const float2 a = Z[(l >> 1) * PN + m];
+        const float2 b = Z[(l >> 1) * PN + (m ? N - m : 0)];
         const float2 Ek = E[m];
         v = (l & 1) ? 0.5f * (Ek.x * (a.y + b.y) - Ek.y * (a.x - b.x))
                     : 0.5f * (Ek.x * (a.x + b.x) + Ek.y * (a.y - b.y));
       } else {
-        const float2 zz = Z[(l >> 1) * N + makhoul_pos(m, N)];
+        const float2 zz = Z[(l >> 1) * PN + makhoul_pos(m, N)];
         v = ((l & 1) ? zz.y : zz.x) / (float)N;
       }
-      dst[base + (long long)l * ls + (long long)m * es] = v;
+      dp[l * ls + m * es] = v;
     }
     __syncthreads();
   }
@@ -361,20 +382,40 @@ __global__ void k32_thomas(Geom g, float* __restrict__ x, float* __restrict__ up
     upper[col] = up;
     float xp = __fdiv_rn(x[col], diag0);
     x[col] = xp;
-    for (int k = 1; k < nz; ++k) {
-      const long long c = (long long)k * P + col;
-      const float denom = __fsub_rn(__fadd_rn(k == nz - 1 ? zdl : zdi, shift), __fmul_rn(off, up));
-      if (k < nz - 1) {
-        up = __fdiv_rn(off, denom);
-        upper[c] = up;
+    // rows are loaded D at a time ahead of the dependent elimination
+    constexpr int D = 8;
+    for (int k0 = 1; k0 < nz; k0 += D) {
+      float xv[D];
+#pragma unroll
+      for (int u = 0; u < D; ++u) xv[u] = k0 + u < nz ? x[(long long)(k0 + u) * P + col] : 0.0f;
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        const int k = k0 + u;
+        if (k >= nz) break;
+        const long long c = (long long)k * P + col;
+        const float denom = __fsub_rn(__fadd_rn(k == nz - 1 ? zdl : zdi, shift), __fmul_rn(off, up));
+        if (k < nz - 1) {
+          up = __fdiv_rn(off, denom);
+          upper[c] = up;
+        }
+        xp = __fdiv_rn(__fsub_rn(xv[u], __fmul_rn(off, xp)), denom);
+        x[c] = xp;
       }
-      xp = __fdiv_rn(__fsub_rn(x[c], __fmul_rn(off, xp)), denom);
-      x[c] = xp;
     }
-    for (int k = nz - 2; k >= 0; --k) {
-      const long long c = (long long)k * P + col;
-      xp = __fsub_rn(x[c], __fmul_rn(upper[c], xp));
-      x[c] = xp;
+    for (int k0 = nz - 2; k0 >= 0; k0 -= D) {
+      float xv[D], uv[D];
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        const long long c = (long long)(k0 - u) * P + col;
+        xv[u] = k0 - u >= 0 ? x[c] : 0.0f;
+        uv[u] = k0 - u >= 0 ? upper[c] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < D; ++u) {
+        if (k0 - u < 0) break;
+        xp = __fsub_rn(xv[u], __fmul_rn(uv[u], xp));
+        x[(long long)(k0 - u) * P + col] = xp;
+      }
     }
   }
 }
@@ -468,15 +509,25 @@ static int f32_stats(etc_plan* pl, double out[10]) {
 }
 
 // line batch size: about 4096 packed complex elements (32 KB) per pass
-static int f32_lp(int N) { return std::max(1, std::min(32, 4096 / std::max(1, N))); }
+static int f32_lp(int N) { return f32_lp_of(std::max(1, N)); }
 
 template <int AX, int INV>
 static int f32_pass(etc_plan* pl, const float* src, float* dst, int pcg) {
   const Geom g = geom(pl);
   const int N = AX == 0 ? pl->nx : pl->ny, nl = AX == 0 ? pl->ny : pl->nx;
   const int LP = f32_lp(N);
-  const size_t smem = 2 * (size_t)LP * N * sizeof(float2);
-  auto kern = k32_lines<AX, INV>;
+  const size_t smem = 2 * (size_t)LP * (N + 1) * sizeof(float2);
+  auto kern = k32_lines<AX, INV, 0>;
+  switch (N) {
+    case 16: kern = k32_lines<AX, INV, 4>; break;
+    case 32: kern = k32_lines<AX, INV, 5>; break;
+    case 64: kern = k32_lines<AX, INV, 6>; break;
+    case 128: kern = k32_lines<AX, INV, 7>; break;
+    case 256: kern = k32_lines<AX, INV, 8>; break;
+    case 512: kern = k32_lines<AX, INV, 9>; break;
+    case 1024: kern = k32_lines<AX, INV, 10>; break;
+    default: break;
+  }
   int rc;
   if (smem > 48 * 1024 && (rc = prep_smem(kern, smem))) return rc;
   const long long work = (long long)pl->nz * ((nl + 2 * LP - 1) / (2 * LP));
@@ -538,6 +589,11 @@ static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max
   CK(cudaMemsetAsync(pl->counters, 0, 64 * sizeof(unsigned), pl->stream));
   CK(cudaEventRecord(pl->ev0, pl->stream));
   const int G = grid1d(pl, pl->n);
+  // stencil: 32x8 column tiles x z chunks, about 8 CTAs per SM
+  const long long tiles = (long long)((pl->nx + 31) / 32) * ((pl->ny + 7) / 8);
+  const int nch = (int)std::max(1LL, std::min<long long>(pl->nz, (long long)pl->sms * 8 / std::max(1LL, tiles)));
+  const int kch = (pl->nz + nch - 1) / nch;
+  const int GS = (int)std::min<long long>(tiles * ((pl->nz + kch - 1) / kch), (long long)pl->sms * 8);
   {
     Tm tm(pl, 6);
     k32_rhs<<<G, 256, 0, pl->stream>>>(g, pl->tb32, (float)p_in, (float)p_out, r, p, pl->ctl, pl->partials,
@@ -560,11 +616,11 @@ static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max
       {
         Tm tm(pl, 0);
         if (it == 1)
-          k32_stencil<true><<<G, 256, 0, pl->stream>>>(g, tx, ty, tz, pl->tb32, zv, nullptr, wn, q, pl->ctl,
-                                                       pl->partials, pl->counters + 0, 1);
-        else
-          k32_stencil<false><<<G, 256, 0, pl->stream>>>(g, tx, ty, tz, pl->tb32, zv, wo, wn, q, pl->ctl,
+          k32_stencil<true><<<GS, 256, 0, pl->stream>>>(g, kch, tx, ty, tz, pl->tb32, zv, nullptr, wn, q, pl->ctl,
                                                         pl->partials, pl->counters + 0, 1);
+        else
+          k32_stencil<false><<<GS, 256, 0, pl->stream>>>(g, kch, tx, ty, tz, pl->tb32, zv, wo, wn, q, pl->ctl,
+                                                         pl->partials, pl->counters + 0, 1);
         CK(cudaGetLastError());
       }
       {

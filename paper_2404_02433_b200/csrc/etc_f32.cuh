@@ -22,7 +22,7 @@
 // this path is the reference's precision study, not the benchmark.  The 2-D
 // transforms run as two line passes (x-lines, then y-lines / the reverse for
 // the inverse), each a batch of pair-packed complex lines in shared memory
-// (radix-2 Stockham FFT for power-of-two lengths, direct DFT otherwise); the z-solve
+// (Stockham FFT, radix-4 stages, for power-of-two lengths; direct DFT otherwise); the z-solve
 // is the reference's Thomas elimination, one thread per mode column, with the
 // elimination coefficients in a scratch vector.
 
@@ -183,16 +183,20 @@ __global__ void __launch_bounds__(256) k32_stencil(Geom g, int kchunk, const flo
     if (i >= nx || j >= ny) continue;
     const int k0 = ch * kchunk, k1 = min(nz, k0 + kchunk);
     const long long col = (long long)j * nx + i;
-    for (int k = k0; k < k1; ++k) {
-      const long long c = (long long)k * P + col;
-      const float u = W(c);
+    // the column's w and tz ride along z in registers (um, u, un; fzm)
+    long long c = (long long)k0 * P + col;
+    float um = k0 > 0 ? W(c - P) : 0.0f, fzm = k0 > 0 ? tz[c - P] : 0.0f;
+    float u = W(c);
+    for (int k = k0; k < k1; ++k, c += P) {
+      const float un = k + 1 < nz ? W(c + P) : 0.0f;
+      const float fz = tz[c];
       float acc = 0.0f;
       if (i > 0) acc = __fadd_rn(acc, __fmul_rn(tx[c - 1], __fsub_rn(u, W(c - 1))));
       if (i + 1 < nx) acc = __fsub_rn(acc, __fmul_rn(tx[c], __fsub_rn(W(c + 1), u)));
       if (j > 0) acc = __fadd_rn(acc, __fmul_rn(ty[c - nx], __fsub_rn(u, W(c - nx))));
       if (j + 1 < ny) acc = __fsub_rn(acc, __fmul_rn(ty[c], __fsub_rn(W(c + nx), u)));
-      if (k > 0) acc = __fadd_rn(acc, __fmul_rn(tz[c - P], __fsub_rn(u, W(c - P))));
-      if (k + 1 < nz) acc = __fsub_rn(acc, __fmul_rn(tz[c], __fsub_rn(W(c + P), u)));
+      if (k > 0) acc = __fadd_rn(acc, __fmul_rn(fzm, __fsub_rn(u, um)));
+      if (k + 1 < nz) acc = __fsub_rn(acc, __fmul_rn(fz, __fsub_rn(un, u)));
       if (k == 0) acc = __fadd_rn(acc, __fmul_rn(tb[col], u));
       if (k == nz - 1) acc = __fadd_rn(acc, __fmul_rn(tb[P + col], u));
       if (wnew) wnew[c] = u;
@@ -200,6 +204,9 @@ __global__ void __launch_bounds__(256) k32_stencil(Geom g, int kchunk, const flo
       dqw = fma((double)acc, (double)u, dqw);
       dqq = fma((double)acc, (double)acc, dqq);
       dww = fma((double)u, (double)u, dww);
+      um = u;
+      u = un;
+      fzm = fz;
     }
   }
   if (!pcg) return;
@@ -207,15 +214,18 @@ __global__ void __launch_bounds__(256) k32_stencil(Geom g, int kchunk, const flo
   grid_sum_finalize<3>(v, partials, counter, [&](double (&t)[3]) { fin_stencil32(ctl, t[0], t[1], t[2]); });
 }
 
-// p += float32(alpha) w, r -= float32(alpha) q, ||r|| (krylov.py:76-84)
-__global__ void k32_update(long long n, float* __restrict__ p, float* __restrict__ r, const float* __restrict__ w,
-                           const float* __restrict__ q, Ctl* ctl, double* partials, unsigned* counter, double* hist) {
+// p += float32(alpha) w, r -= float32(alpha) q, ||r|| (krylov.py:76-84).
+// homogenize observes p only through the outflow flux (tpfa.py:234-258), so
+// p is updated from cell p0 on: the last plane (as the f64 path does).
+__global__ void k32_update(long long n, long long p0, float* __restrict__ p, float* __restrict__ r,
+                           const float* __restrict__ w, const float* __restrict__ q, Ctl* ctl, double* partials,
+                           unsigned* counter, double* hist) {
   if (ctl->done) return;
   const float af = (float)ctl->alpha;
   double rr = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += stride) {
-    p[c] = __fadd_rn(p[c], __fmul_rn(af, w[c]));
+    if (c >= p0) p[c] = __fadd_rn(p[c], __fmul_rn(af, w[c]));
     const float v = __fsub_rn(r[c], __fmul_rn(af, q[c]));
     r[c] = v;
     rr = fma((double)v, (double)v, rr);
@@ -300,7 +310,58 @@ __global__ void __launch_bounds__(256) k32_lines(Geom g, const float* src, float
     // ---- FFT of the LP packed lines in A (natural order in and out);
     // tw is exp(-2 pi i m/N), the inverse uses its conjugate
     float2* Z = A;
-    if (pow2) {  // radix-2 Stockham auto-sort, ping-pong A <-> B
+    if (LG >= 2) {  // Stockham auto-sort, radix-4 stages (then one radix-2 if LG is odd), ping-pong A <-> B
+      float2 *x = A, *y = B;
+#pragma unroll
+      for (int st = 0; st + 1 < LG; st += 2) {
+        const int Ns = 1 << st;
+        const int tstep = N / (4 * Ns);
+        for (int e = tid; e < LP * (N / 4); e += nt) {
+          const int f = e / (N / 4), j = e - f * (N / 4);
+          const int k = j & (Ns - 1);
+          float2 v[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            v[r] = x[f * PN + j + r * (N / 4)];
+            if (r) {
+              float2 w = tw[r * k * tstep];
+              if (INV) w.y = -w.y;
+              v[r] = c32mul(v[r], w);
+            }
+          }
+          // 4-point DFT; forward uses -i, the inverse +i
+          const float2 s02 = make_float2(v[0].x + v[2].x, v[0].y + v[2].y);
+          const float2 d02 = make_float2(v[0].x - v[2].x, v[0].y - v[2].y);
+          const float2 s13 = make_float2(v[1].x + v[3].x, v[1].y + v[3].y);
+          const float2 d13 = make_float2(v[1].x - v[3].x, v[1].y - v[3].y);
+          const float2 jd = INV ? make_float2(-d13.y, d13.x) : make_float2(d13.y, -d13.x);  // (+-i) d13
+          const int d = f * PN + ((j - k) << 2) + k;
+          y[d] = make_float2(s02.x + s13.x, s02.y + s13.y);
+          y[d + Ns] = make_float2(d02.x + jd.x, d02.y + jd.y);
+          y[d + 2 * Ns] = make_float2(s02.x - s13.x, s02.y - s13.y);
+          y[d + 3 * Ns] = make_float2(d02.x - jd.x, d02.y - jd.y);
+        }
+        __syncthreads();
+        float2* tmp = x; x = y; y = tmp;
+      }
+      if (LG & 1) {
+        const int Ns = N / 2;
+        for (int e = tid; e < LP * (N / 2); e += nt) {
+          const int f = e / (N / 2), j = e - f * (N / 2);
+          const int k = j & (Ns - 1);
+          float2 w = tw[k];
+          if (INV) w.y = -w.y;
+          const float2 a = x[f * PN + j];
+          const float2 t = c32mul(x[f * PN + j + N / 2], w);
+          const int d = f * PN + ((j - k) << 1) + k;
+          y[d] = make_float2(a.x + t.x, a.y + t.y);
+          y[d + Ns] = make_float2(a.x - t.x, a.y - t.y);
+        }
+        __syncthreads();
+        x = y;
+      }
+      Z = x;
+    } else if (pow2) {  // radix-2 Stockham auto-sort, ping-pong A <-> B
       float2 *x = A, *y = B;
 #pragma unroll
       for (int st = 0; st < (LG ? LG : 31); ++st) {
@@ -625,8 +686,8 @@ static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max
       }
       {
         Tm tm(pl, 1);
-        k32_update<<<G, 256, 0, pl->stream>>>(pl->n, p, r, wn, q, pl->ctl, pl->partials, pl->counters + 1,
-                                              pl->hist);
+        k32_update<<<G, 256, 0, pl->stream>>>(pl->n, (long long)(pl->nz - 1) * g.plane, p, r, wn, q, pl->ctl,
+                                              pl->partials, pl->counters + 1, pl->hist);
         CK(cudaGetLastError());
       }
       if (!none && (rc = f32_precond(pl, r, q, z, 1))) return rc;

@@ -182,3 +182,23 @@ def test_oracle_channels_generator_and_solves(golden_channels):
                            ref_mode=case["ref_mode"], precond=case["precond"])
         assert abs(out["iterations"] - case["iterations"]) <= 1, case["iterations"]
         assert abs(out["kappa_eff"] - case["kappa_eff"]) <= 1e-8 * abs(case["kappa_eff"])
+
+
+def test_oracle_f32_solves_match_reference(golden_f32):
+    """The oracle run on float32 arrays is the reference's precision="f32"
+    path (dtype threaded through scale, faces, transforms, tables, Thomas,
+    PCG; tests/golden/solves_f32.json): same iteration counts, kappa_eff
+    within 1e-5, or twice the reference's own f32-vs-f64 distance where single
+    precision resolves kappa_eff more coarsely (measured 9e-7 on the random
+    RVEs, 1.8e-5 on the contrast-100 center ball whose f32/f64 gap is
+    1.65e-5; float32 dots and pocketfft builds differ in rounding only)."""
+    for case in golden_f32:
+        n = case["n"]
+        if n > 32 or case["precond"] != "fct":
+            continue
+        k = (O.random_balls(n, 40, 0.05, 0.15, case["kappa"], 11) if case["kind"] == "random-a"
+             else O.center_ball(n, case["kappa"])).astype(np.float32)
+        r = O.homogenize(k, k, k, (n, n, n, 1.0, 1.0, 1.0), case["axis"], 1.0, 0.0, case["rtol"])
+        assert r["iterations"] == case["iterations"], (case["kind"], n, case["axis"])
+        gap = abs(case["kappa_eff"] - case["f64_kappa_eff"]) / case["f64_kappa_eff"]
+        assert abs(r["kappa_eff"] - case["kappa_eff"]) <= max(1e-5, 2 * gap) * case["kappa_eff"]

@@ -47,7 +47,8 @@ from .solver import PcgBreakdownError, SolveReport, _BREAKDOWN_MSG, _check, _tor
 
 FIN_STENCIL, FIN_NORMB, FIN_UPDATE, FIN_THOMAS = 0, 1, 2, 3
 (SLAB_FACES, SLAB_STATS, SLAB_NORMB, SLAB_FINALIZE, SLAB_STENCIL, SLAB_UPDATE, SLAB_PACK,
- SLAB_ZSOLVE, SLAB_UNPACK, SLAB_INVERSE, SLAB_PUPDATE, SLAB_FLUX) = range(12)
+ SLAB_ZSOLVE, SLAB_UNPACK, SLAB_INVERSE, SLAB_PUPDATE, SLAB_FLUX,
+ SLAB_ZSUB_TABS, SLAB_ZSUB_ENDS, SLAB_ZSUB_SOLVE) = range(15)
 
 
 def slab_bounds(nzg: int, size: int, rank: int) -> tuple[int, int]:
@@ -81,6 +82,11 @@ class TorchComm:
 
     def alltoall(self, out, inp):
         self.td.all_to_all_single(out, inp, group=self.group)
+
+    def allgather(self, out, inp):
+        """out = [rank 0's inp, rank 1's inp, ...]"""
+        n = inp.numel()
+        self.td.all_gather([out[r * n:(r + 1) * n] for r in range(self.size)], inp, group=self.group)
 
     def barrier(self):
         # peer stores were issued on the current stream: complete them first
@@ -190,6 +196,14 @@ class ThreadComm:
         n = inp.numel() // self.size
         for s in range(self.size):
             out[s * n:(s + 1) * n].copy_(self.hub.slots[s][self.rank * n:(self.rank + 1) * n])
+        self._sync()
+
+    def allgather(self, out, inp):
+        self.hub.slots[self.rank] = inp
+        self._sync()
+        n = inp.numel()
+        for s in range(self.size):
+            out[s * n:(s + 1) * n].copy_(self.hub.slots[s])
         self._sync()
 
     def neighbours(self, lo, hi, recv_lo, recv_hi):
@@ -328,7 +342,7 @@ def _exchange_planes(ops, comm, which: int, nzl: int):
 
 
 def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_mode="opt",
-               max_iter=1024, check_every=1, p2p=None) -> SolveReport:
+               max_iter=1024, check_every=1, p2p=None, zsolve=None) -> SolveReport:
     """PCG on this rank's z-slab of the canonical field (kx, ky, kz: local
     planes, x-fastest).  grid = (nx, ny, nzg, lx, ly, lz), the canonical
     global grid.  Every rank returns the same report.
@@ -338,9 +352,26 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
     stores into the destination ranks' pencil buffers, the z-solve into the
     owners' return buffers; halo planes are stored into the neighbours' halo
     planes), where the plan supports it (etc_slab_p2p_ok) and the comm can
-    share device pointers (same process, or CUDA IPC)."""
+    share device pointers (same process, or CUDA IPC).
+
+    zsolve (default: ETC_ZSOLVE in the environment, else "pencil"): "pencil"
+    moves the spectrum through two all-to-alls so that every z-column is
+    solved whole on one rank; "spike" solves each rank's block of every
+    column in place (substructured tridiagonal): the ranks
+    exchange only the two end values of their block solutions per column
+    (an all-gather of 2·nx·ny doubles per rank) and every rank solves the
+    small reduced system of the block-boundary unknowns."""
     nx, ny, nzg, lx, ly, lz = grid
     nzl = nzg // comm.size
+    if zsolve is None:
+        import os
+
+        zsolve = os.environ.get("ETC_ZSOLVE", "pencil")
+    if zsolve not in ("pencil", "spike"):
+        raise ValueError(f"zsolve must be 'pencil' or 'spike', not {zsolve!r}")
+    spike = zsolve == "spike"
+    if spike:
+        p2p = False
     iso = kx is ky and ky is kz
     ops.load(kx, ky, kz)
     if p2p is None:
@@ -390,6 +421,8 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
     wx, wy, zd = eigen_weights(nx), eigen_weights(ny), z_chain_diagonal(nzg, refs)
     check_pivots(nzg, zd, refs)
     ops.set_reference(refs, wx, wy, zd)
+    if spike:
+        ops.run(SLAB_ZSUB_TABS)  # every block's spike end values (matrix only, once per solve)
 
     xbuf = ops.new(8)
     xbuf.zero_()
@@ -404,9 +437,21 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
     # on the fused path the forward transform writes its spectrum straight
     # into the all-to-all send buffer and the inverse reads it back from there
     # (pack / unpack fused into the transforms)
-    spec = None if use_p2p else (send if fused else None)
+    spec = None if (use_p2p or spike) else (send if fused else None)
+    if spike:
+        ends = ops.new(2 * nx * ny)
+        ends_all = ops.new(2 * nx * ny * comm.size)
 
     def zsolve_and_back(first):
+        if spike:
+            ops.run(SLAB_ZSUB_ENDS, 0, ends)            # g_first, g_last of the local block solves
+            comm.allgather(ends_all, ends)
+            ops.run(SLAB_ZSUB_SOLVE, 0, ends_all)       # reduced system, then the coupled block solve
+            comm.allreduce(xbuf[4:5])
+            ops.run(SLAB_FINALIZE, FIN_THOMAS)
+            ops.run(SLAB_INVERSE, 1 if first else 2, None)
+            _exchange_planes(ops, comm, 4 if fused else 3, nzl)
+            return
         if use_p2p:
             # the forward stage stored the spectrum into the peers' pencil
             # buffers; the scalar all-reduce after it was the barrier
@@ -461,7 +506,7 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
 
 
 def virtual_slab_solve(field_cube, grid, nranks: int, p_in=1.0, p_out=0.0, rtol=1e-9, ref_mode="opt",
-                       max_iter=1024, device=None, p2p=None) -> list:
+                       max_iter=1024, device=None, p2p=None, zsolve=None) -> list:
     """Run the z-slab solve with `nranks` virtual ranks on one GPU (threads +
     device copies stand in for NCCL); field_cube: canonical (nzg, ny, nx)
     CUDA tensor (isotropic field).  Returns every rank's report."""
@@ -480,7 +525,8 @@ def virtual_slab_solve(field_cube, grid, nranks: int, p_in=1.0, p_out=0.0, rtol=
             k0, nzl = slab_bounds(nzg, nranks, r)
             k = field_cube[k0:k0 + nzl].contiguous().reshape(-1)
             ops = CudaSlabOps(nx, ny, nzg, k0, nzl, nranks, r, lx, ly, lz, dev)
-            out[r] = slab_solve(ops, comms[r], k, k, k, grid, p_in, p_out, rtol, ref_mode, max_iter, p2p=p2p)
+            out[r] = slab_solve(ops, comms[r], k, k, k, grid, p_in, p_out, rtol, ref_mode, max_iter, p2p=p2p,
+                                zsolve=zsolve)
         except BaseException as exc:  # surface worker failures
             errs.append(exc)
             comms[r].hub.barrier.abort()

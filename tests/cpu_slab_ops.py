@@ -270,6 +270,82 @@ class CpuSlabOps:
             s = float(np.sum((tout * hz) * (self.p[kl] - self.p_out)))
         ext[0] = s
 
+    # -- substructured ("spike") z-solve: stages 12-14 -----------------------
+    def _diag(self, kg):
+        return self.zd[kg] + self.shift
+
+    def _stage12(self, arg, ext):  # spike end values of every block (matrix only)
+        m, P, off = self.nzl, self.size, self.off
+        self.sp = []
+        for p in range(P):
+            r = 1.0 / self._diag(p * m)
+            y = r.copy()  # forward elimination of e_0
+            for k in range(1, m):
+                r = 1.0 / (self._diag(p * m + k) - off * off * r)
+                y = -off * y * r
+            rb = 1.0 / self._diag(p * m + m - 1)
+            for k in range(m - 2, -1, -1):
+                rb = 1.0 / (self._diag(p * m + k) - off * off * rb)
+            # V = A_p^-1 (off e_0), W = A_p^-1 (off e_last): first/last entries
+            self.sp.append((off * rb, off * y, off * r))  # V_f, V_l (= W_f), W_l
+
+    def _block_solve(self, d, top, bot):
+        """A_p x = d - off top e_0 - off bot e_last (top-down elimination)."""
+        m, off, k0 = self.nzl, self.off, self.k0
+        d = d.copy()
+        d[0] = d[0] - off * top
+        d[m - 1] = d[m - 1] - off * bot
+        rp = np.empty_like(d)
+        rp[0] = 1.0 / self._diag(k0)
+        d[0] = d[0] * rp[0]
+        for k in range(1, m):
+            rp[k] = 1.0 / (self._diag(k0 + k) - off * off * rp[k - 1])
+            d[k] = (d[k] - off * d[k - 1]) * rp[k]
+        for k in range(m - 2, -1, -1):
+            d[k] = d[k] - off * rp[k] * d[k + 1]
+        return d
+
+    def _stage13(self, arg, ext):  # g = A_p^-1 t: first and last values -> ext
+        if self.ctl.done:
+            return
+        g = self._block_solve(self.t, 0.0, 0.0)
+        ext.copy_(torch.from_numpy(np.concatenate([g[0].reshape(-1), g[-1].reshape(-1)])))
+
+    def _stage14(self, arg, ext):  # reduced system of the block-boundary values, coupled block solve
+        if self.ctl.done:
+            return
+        P, me, plane = self.size, self.rank, self.nx * self.ny
+        e = ext.numpy().reshape(P, 2, self.ny, self.nx)
+        top = np.zeros((self.ny, self.nx))
+        bot = np.zeros((self.ny, self.nx))
+        if P > 1:
+            n = 2 * (P - 1)  # unknowns b_0, a_1, b_1, a_2, ..., b_{P-2}, a_{P-1}
+            M = np.zeros((self.ny, self.nx, n, n))
+            rhs = np.zeros((self.ny, self.nx, n))
+            for p in range(P - 1):
+                vf, vl, wl = self.sp[p]
+                M[..., 2 * p, 2 * p] = 1.0  # b_p + V_l(p) b_{p-1} + W_l(p) a_{p+1} = g_l(p)
+                if p > 0:
+                    M[..., 2 * p, 2 * p - 2] = vl
+                M[..., 2 * p, 2 * p + 1] = wl
+                rhs[..., 2 * p] = e[p, 1]
+                vf1, vl1, _ = self.sp[p + 1]  # a_{p+1} + V_f(p+1) b_p + W_f(p+1) a_{p+2} = g_f(p+1)
+                M[..., 2 * p + 1, 2 * p + 1] = 1.0
+                M[..., 2 * p + 1, 2 * p] = vf1
+                if p + 1 < P - 1:
+                    M[..., 2 * p + 1, 2 * p + 3] = vl1
+                rhs[..., 2 * p + 1] = e[p + 1, 0]
+            sol = np.linalg.solve(M, rhs[..., None])[..., 0]
+            if me > 0:
+                top = sol[..., 2 * (me - 1)]
+            if me < P - 1:
+                bot = sol[..., 2 * me + 1]
+        x = self._block_solve(self.t, top, bot)
+        ax = np.where(np.arange(self.nx) == 0, 0.5, 1.0)
+        ay = np.where(np.arange(self.ny) == 0, 0.5, 1.0)
+        self.xbuf[4] = float(np.sum(ay[:, None] * ax[None, :] * self.t * x))
+        self.t = x
+
     def status(self, max_iter):
         c = self.ctl
         info = SimpleNamespace(iterations=c.it, converged=c.converged, status=c.status, breakdown_iter=c.bd_iter,

@@ -66,7 +66,7 @@ def _primitives(rank, size, port, q):
             td.destroy_process_group()
 
 
-def _solve(rank, size, port, q, n, C, axis, fused=False):
+def _solve(rank, size, port, q, n, C, axis, fused=False, zsolve="pencil"):
     try:
         _init(rank, size, port)
         from cpu_slab_ops import CpuSlabOps
@@ -80,7 +80,7 @@ def _solve(rank, size, port, q, n, C, axis, fused=False):
         sl = lambda a: torch.from_numpy(np.ascontiguousarray(a[k0:k0 + nzl]).reshape(-1))
         ops = CpuSlabOps(g[0], g[1], g[2], k0, nzl, size, rank, g[3], g[4], g[5], fused=fused)
         t = sl(kx)
-        rep = slab_solve(ops, comm, t, t, t, g, 1.0, 0.0, 1e-8)
+        rep = slab_solve(ops, comm, t, t, t, g, 1.0, 0.0, 1e-8, zsolve=zsolve)
         q.put((rank, (rep.iterations, rep.kappa_eff, rep.relative_residuals), None))
     except Exception as exc:  # pragma: no cover
         import traceback
@@ -110,16 +110,21 @@ def test_comm_primitives(size):
         assert ok, (rank, err)
 
 
-@pytest.mark.parametrize("size,n,C,axis,fused", [(2, 16, 100.0, "z", False), (4, 16, 10.0, "x", False),
-                                                 (2, 24, 100.0, "y", False), (2, 16, 100.0, "z", True),
-                                                 (4, 16, 10.0, "y", True)])
-def test_slab_solve_matches_single_process(size, n, C, axis, fused):
+@pytest.mark.parametrize("size,n,C,axis,fused,zsolve", [(2, 16, 100.0, "z", False, "pencil"),
+                                                        (4, 16, 10.0, "x", False, "pencil"),
+                                                        (2, 24, 100.0, "y", False, "pencil"),
+                                                        (2, 16, 100.0, "z", True, "pencil"),
+                                                        (4, 16, 10.0, "y", True, "pencil"),
+                                                        (2, 16, 100.0, "z", True, "spike"),
+                                                        (4, 16, 100.0, "x", False, "spike"),
+                                                        (4, 24, 10.0, "y", True, "spike")])
+def test_slab_solve_matches_single_process(size, n, C, axis, fused, zsolve):
     sys.path.insert(0, str(ROOT))
     from oracle import etc_oracle as O
 
     k = O.random_balls(n, 40, 0.05, 0.15, C, 11)
     ref = O.homogenize(k, k, k, (n, n, n, 1.0, 1.0, 1.0), axis, 1.0, 0.0, 1e-8)
-    res = _spawn(_solve, size, n, C, axis, fused)
+    res = _spawn(_solve, size, n, C, axis, fused, zsolve)
     for rank, out, err in res:
         assert err is None, err
         it, kappa, hist = out

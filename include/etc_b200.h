@@ -163,7 +163,13 @@ int etc_profile_read(etc_plan* plan, double ms[8], long long counts[8], int rese
  * first transform, 3 finalize (arg: 0 stencil, 1 ||b||, 2 update, 3 z-solve),
  * 4 stencil (arg = iteration), 5 r update + transform, 6 pack (ext = send),
  * 7 z-solve (ext = pencil), 8 unpack (ext = received), 9 inverse transform,
- * 10 final p update (arg = last iteration), 11 outflow flux (ext = 1 double).
+ * 10 final p update (arg = last iteration), 11 outflow flux (ext = 1 double),
+ * substructured z-solve instead of 6-8 (replaces the pencil
+ * all-to-alls, preconditioner.py:215-250 on each rank's block of rows):
+ * 12 spike tables (once per solve, after etc_set_reference; nranks <= 8),
+ * 13 block end values g_first/g_last (ext = 2 nx ny doubles, this rank's),
+ * 14 reduced system + coupled block solve in place (ext = all ranks' stage-13
+ * outputs, all-gathered: nranks x 2 nx ny doubles).
  * Same kernels as the single-GPU path; krylov.py:56-90 semantics. */
 int etc_slab_create(etc_plan** out, int nx, int ny, int nzg, int k0, int nzl, int nranks, int rank,
                     double lx, double ly, double lz, void* stream);

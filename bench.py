@@ -232,7 +232,7 @@ def run_b200(args, rank, world, local_rank):
         comm = D.TorchComm()
 
         def step(fld=field):
-            return D.effective_tensor_dist(fld, comm, rtol=args.rtol, axes=axes, device=dev)
+            return D.effective_tensor_dist(fld, comm, rtol=args.rtol, axes=axes, device=dev, zsolve=args.zsolve)
     else:
         def step(fld=field):
             return P.effective_tensor(fld, rtol=args.rtol, axes=axes, device=dev)
@@ -298,10 +298,15 @@ def run_b200(args, rank, world, local_rank):
     kms = [pms[i] / args.steps for i in range(8)]  # per-kernel totals per timed step
     kcnt = [cnts[i] / args.steps for i in range(8)]
     N = n ** 3 // world  # cells per rank per launch
-    wfuse = (not dist and not args.slab and os.environ.get("ETC_WFUSE", "1") != "0" and n >= 128
-             and n & (n - 1) == 0)
+    # z-slab ranks run the same fused kernels (etc_slab_fused: ny / P a power of two >= 2)
+    wfuse = (os.environ.get("ETC_WFUSE", "1") != "0" and n >= 128 and n & (n - 1) == 0
+             and (not dist or n // world >= 2))
     phases = wfuse and os.environ.get("ETC_PHASES", "1") != "0"  # the bench field has two phases
     bpc = bytes_per_cell(wfuse, phases)
+    if dist and args.zsolve == "spike":
+        # k_zsub_ends reads the slab twice (16 B/cell); k_zsub_solve moves t r/w, d' w/r and the
+        # pivot table r (48 B/cell): 32 B/cell per launch on average
+        bpc["zsolve"] = 32
     peaks = load_peaks()
     kern = {}
     for i, name in enumerate(KCLASS):
@@ -396,7 +401,8 @@ def run_b200(args, rank, world, local_rank):
             "n": n, "contrast": args.contrast, "rtol": args.rtol, "directions": axes,
             "iterations": iters, "ms_per_iter": round(ms_step / max(1, total_iters), 4),
             "kappa_eff": {a: reps[a].kappa_eff for a in axes},
-            "parallelism": f"z-slab x{world} (NCCL halo + pencil all-to-all + all-reduce)" if dist
+            "parallelism": (f"z-slab x{world} (NCCL halo + pencil all-to-all + all-reduce)" if args.zsolve == "pencil"
+                            else f"z-slab x{world} (NCCL halo + spike z-solve all-gather + all-reduce)") if dist
                            else "single",
             "l2": "inputs larger than L2 (one f64 vector = %.2f GB)" % (8 * N / 1e9),
         },
@@ -492,8 +498,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slab", action="store_true", help="z-slab path even on one rank (exercises NCCL plumbing)")
+    ap.add_argument("--zsolve", choices=["pencil", "spike"], default=None,
+                    help="z-slab z-solve: pencil all-to-alls, or the substructured spike solve (default for N > 1)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.zsolve is None:
+        args.zsolve = "spike" if world > 1 else "pencil"
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

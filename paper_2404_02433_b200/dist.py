@@ -80,12 +80,26 @@ class TorchComm:
         ops = {"sum": self.td.ReduceOp.SUM, "min": self.td.ReduceOp.MIN, "max": self.td.ReduceOp.MAX}
         self.td.all_reduce(t, op=ops[op], group=self.group)
 
+    def _gloo_cuda(self, t) -> bool:
+        """gloo moves host memory only: CUDA tensors are staged through the host"""
+        return t.is_cuda and self.td.get_backend(self.group) == "gloo"
+
     def alltoall(self, out, inp):
+        if self._gloo_cuda(inp):
+            host = out.cpu()
+            self.td.all_to_all_single(host, inp.cpu(), group=self.group)
+            out.copy_(host)
+            return
         self.td.all_to_all_single(out, inp, group=self.group)
 
     def allgather(self, out, inp):
         """out = [rank 0's inp, rank 1's inp, ...]"""
         n = inp.numel()
+        if self._gloo_cuda(inp):
+            host = out.cpu()
+            self.td.all_gather([host[r * n:(r + 1) * n] for r in range(self.size)], inp.cpu(), group=self.group)
+            out.copy_(host)
+            return
         self.td.all_gather([out[r * n:(r + 1) * n] for r in range(self.size)], inp, group=self.group)
 
     def barrier(self):
@@ -113,6 +127,12 @@ class TorchComm:
         """send lo -> rank-1 (its upper halo), hi -> rank+1 (its lower halo);
         receive rank-1's hi into recv_lo and rank+1's lo into recv_hi."""
         td, r, p = self.td, self.rank, self.size
+        if self._gloo_cuda(lo):
+            hl, hh, rl, rh = lo.cpu(), hi.cpu(), recv_lo.cpu(), recv_hi.cpu()
+            self.neighbours(hl, hh, rl, rh)
+            recv_lo.copy_(rl)
+            recv_hi.copy_(rh)
+            return
         ops = []
         if r > 0:
             ops += [td.P2POp(td.isend, lo, r - 1, self.group), td.P2POp(td.irecv, recv_lo, r - 1, self.group)]
@@ -565,11 +585,13 @@ def _canonical(fld, axis: str):
 
 
 def effective_tensor_dist(field, comm=None, rtol: float = 1e-9, p_in: float = 1.0, p_out: float = 0.0,
-                          ref_mode: str = "opt", max_iter: int = 1024, axes: str = "xyz", device=None):
+                          ref_mode: str = "opt", max_iter: int = 1024, axes: str = "xyz", device=None,
+                          zsolve=None):
     """Multi-GPU effective_tensor: every rank passes the same field (host
     numpy or CUDA tensors); each solves its z-slab of every load direction
     with the others over `comm` (default: torch.distributed world).  Returns
-    (kappa[3], {axis: SolveReport}) on every rank."""
+    (kappa[3], {axis: SolveReport}) on every rank.  zsolve: "pencil" or
+    "spike" (see slab_solve)."""
     torch = _torch()
     from .solver import _as_field
 
@@ -601,6 +623,7 @@ def effective_tensor_dist(field, comm=None, rtol: float = 1e-9, p_in: float = 1.
         if ops is None:
             ops = CudaSlabOps(nx, ny, nzg, k0, nzl, comm.size, comm.rank, grid[3], grid[4], grid[5], dev)
             _OPS_CACHE[key] = ops
-        reports[ax] = slab_solve(ops, comm, kx, ky, kz, grid, p_in, p_out, rtol, ref_mode, max_iter)
+        reports[ax] = slab_solve(ops, comm, kx, ky, kz, grid, p_in, p_out, rtol, ref_mode, max_iter,
+                                 zsolve=zsolve)
     kappa = np.array([reports[a].kappa_eff if a in reports else np.nan for a in "xyz"])
     return kappa, reports

@@ -27,7 +27,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank(rank, size, port, n, q):
+def _rank(rank, size, port, n, q, zsolve="pencil"):
     try:
         sys.path.insert(0, str(ROOT))
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -45,8 +45,10 @@ def _rank(rank, size, port, n, q):
         k = f.kx.reshape(n, n, n)[k0:k0 + nzl].contiguous().reshape(-1)
         ops = dist.CudaSlabOps(n, n, n, k0, nzl, size, rank, 1.0, 1.0, 1.0)
         comm = dist.TorchComm()
-        rep = dist.slab_solve(ops, comm, k, k, k, (n, n, n, 1.0, 1.0, 1.0), 1.0, 0.0, 1e-8, p2p=True)
-        q.put((rank, (rep.iterations, rep.kappa_eff, rep.relative_residuals, ops.p2p_ok()), None))
+        rep = dist.slab_solve(ops, comm, k, k, k, (n, n, n, 1.0, 1.0, 1.0), 1.0, 0.0, 1e-8,
+                              p2p=zsolve == "pencil", zsolve=zsolve)
+        q.put((rank, (rep.iterations, rep.kappa_eff, rep.relative_residuals,
+                      ops.p2p_ok() or zsolve == "spike"), None))
         td.destroy_process_group()
     except Exception:  # pragma: no cover
         import traceback
@@ -54,7 +56,10 @@ def _rank(rank, size, port, n, q):
         q.put((rank, None, traceback.format_exc()))
 
 
-def test_two_processes_peer_exchange_over_ipc():
+@pytest.mark.parametrize("zsolve", ["pencil", "spike"])
+def test_two_processes_peer_exchange_over_ipc(zsolve):
+    """pencil: the peer-memory exchange over IPC; spike: the substructured
+    z-solve with its end values all-gathered by TorchComm (gloo)."""
     import torch.multiprocessing as mp
 
     sys.path.insert(0, str(ROOT))
@@ -64,10 +69,14 @@ def test_two_processes_peer_exchange_over_ipc():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, size, port, n, q)) for r in range(size)]
+    procs = [ctx.Process(target=_rank, args=(r, size, port, n, q, zsolve)) for r in range(size)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
+    res = []
+    for _ in procs:
+        res.append(q.get(timeout=300))
+        assert res[-1][2] is None, res[-1][2]
+    res.sort(key=lambda x: x[0])
     for p in procs:
         p.join(timeout=60)
     for rank, out, err in res:

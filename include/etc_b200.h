@@ -192,8 +192,9 @@ int etc_slab_fused(etc_plan* plan);
 /* Peer exchange (fused all-to-all over peer memory): 1 if this slab plan
  * can run it (fused path, exact-fit z-solve on the pencil). */
 int etc_slab_p2p_ok(etc_plan* plan);
-/* The plan's exchange buffers (device, nzl*ny*nx doubles each, allocated on
- * first request): which 0 = pencil (recv) buffer, 1 = return buffer. */
+/* The plan's exchange buffers (device, allocated on first request):
+ * which 0 = pencil (recv) buffer, 1 = return buffer (nzl*ny*nx doubles
+ * each), 2 = the spike z-solve's end values of all ranks (nranks*2*ny*nx). */
 int etc_slab_xbuf(etc_plan* plan, int which, double** out);
 /* Every rank's pencil and return buffers as pointers valid in this process
  * (own, same-process, or CUDA-IPC-opened), nranks entries each; NULL turns
@@ -202,6 +203,12 @@ int etc_slab_xbuf(etc_plan* plan, int which, double** out);
  * its rows into the owners' return buffers (no all-to-all); the host's
  * following scalar all-reduce is the barrier. */
 int etc_slab_set_peers(etc_plan* plan, double* const* recv_peers, double* const* back_peers);
+/* Spike z-solve over peer memory: SLAB_ZSUB_ENDS stores this rank's end
+ * values into slot `rank` of every rank's etc_slab_xbuf(plan, 2, ...) buffer
+ * (nranks x 2 nx ny doubles; device pointers valid in this process, own or
+ * IPC-opened), replacing the host all-gather; SLAB_ZSUB_SOLVE with ext = NULL
+ * reads the own buffer.  NULL table: back to the all-gather. */
+int etc_slab_set_ends_peers(etc_plan* plan, double* const* ends_peers);
 /* Device address of plane `plane` (-1..nzl) of buffer `which` (as
  * etc_slab_plane): the target of the peers' halo-plane stores. */
 int etc_slab_plane_ptr(etc_plan* plan, int which, int plane, double** out);

@@ -26,7 +26,7 @@ EXPORTS = (
     "etc_apply_precond", "etc_build_rhs", "etc_profile", "etc_profile_read",
     "etc_voxelize_balls", "etc_voxelize_fibres", "etc_fill_channels", "etc_slab_create", "etc_slab_load", "etc_slab_plane",
     "etc_slab_init", "etc_slab_run", "etc_slab_status", "etc_slab_fused", "etc_slab_p2p_ok", "etc_slab_xbuf",
-    "etc_slab_set_peers", "etc_slab_plane_ptr", "etc_ipc_handle", "etc_ipc_open", "etc_ipc_close",
+    "etc_slab_set_peers", "etc_slab_set_ends_peers", "etc_slab_plane_ptr", "etc_ipc_handle", "etc_ipc_open", "etc_ipc_close",
 )
 
 
@@ -93,6 +93,7 @@ _SIGS = {
     "etc_slab_p2p_ok": (_I, [_P]),
     "etc_slab_xbuf": (_I, [_P, _I, C.POINTER(_P)]),
     "etc_slab_set_peers": (_I, [_P, C.POINTER(_P), C.POINTER(_P)]),
+    "etc_slab_set_ends_peers": (_I, [_P, C.POINTER(_P)]),
     "etc_slab_plane_ptr": (_I, [_P, _I, _I, C.POINTER(_P)]),
     "etc_ipc_handle": (_I, [_P, _P, _P, C.POINTER(C.c_size_t)]),
     "etc_ipc_open": (_I, [_P, C.POINTER(_P)]),

@@ -321,6 +321,10 @@ class CudaSlabOps:
         _check(self.lib.etc_ipc_handle(self._h, C.c_void_p(ptr), buf, C.byref(off)), "etc_ipc_handle")
         return bytes(buf.raw), int(off.value)
 
+    def set_ends_peers(self, ptrs):
+        arr = C.c_void_p * len(ptrs)
+        _check(self.lib.etc_slab_set_ends_peers(self._h, arr(*ptrs)), "etc_slab_set_ends_peers")
+
     def set_peers(self, recv_ptrs, back_ptrs):
         arr = C.c_void_p * len(recv_ptrs)
         _check(self.lib.etc_slab_set_peers(self._h, arr(*recv_ptrs), arr(*back_ptrs)), "etc_slab_set_peers")
@@ -390,7 +394,14 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
     if zsolve not in ("pencil", "spike"):
         raise ValueError(f"zsolve must be 'pencil' or 'spike', not {zsolve!r}")
     spike = zsolve == "spike"
+    spike_p2p = False
     if spike:
+        if p2p is None:
+            import os
+
+            p2p = os.environ.get("ETC_P2P", "0") == "1"
+        # the end values go to the peers by stores from k_zsub_ends (no all-gather)
+        spike_p2p = bool(p2p) and hasattr(comm, "share_pointers") and hasattr(ops, "set_ends_peers")
         p2p = False
     iso = kx is ky and ky is kz
     ops.load(kx, ky, kz)
@@ -461,12 +472,21 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
     if spike:
         ends = ops.new(2 * nx * ny)
         ends_all = ops.new(2 * nx * ny * comm.size)
+        if spike_p2p:
+            table = comm.share_pointers(ops, [ops.xbuf(2)])
+            ops.set_ends_peers([t[0] for t in table])
+            fence = ops.new(1)
 
     def zsolve_and_back(first):
         if spike:
-            ops.run(SLAB_ZSUB_ENDS, 0, ends)            # g_first, g_last of the local block solves
-            comm.allgather(ends_all, ends)
-            ops.run(SLAB_ZSUB_SOLVE, 0, ends_all)       # reduced system, then the coupled block solve
+            if spike_p2p:
+                ops.run(SLAB_ZSUB_ENDS, 0, None)        # stored into every rank's end-value buffer
+                comm.allreduce(fence)                   # ... a one-element all-reduce is the barrier
+                ops.run(SLAB_ZSUB_SOLVE, 0, None)
+            else:
+                ops.run(SLAB_ZSUB_ENDS, 0, ends)        # g_first, g_last of the local block solves
+                comm.allgather(ends_all, ends)
+                ops.run(SLAB_ZSUB_SOLVE, 0, ends_all)   # reduced system, then the coupled block solve
             comm.allreduce(xbuf[4:5])
             ops.run(SLAB_FINALIZE, FIN_THOMAS)
             ops.run(SLAB_INVERSE, 1 if first else 2, None)

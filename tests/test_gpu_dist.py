@@ -96,3 +96,20 @@ def test_virtual_slabs_spike_zsolve(n, nranks, axis, C):
         big = s > 1e-2
         assert np.all(np.abs(h[big] - s[big]) <= 1e-8 * s[big])
         assert rep.ref_params == single.ref_params
+
+
+@pytest.mark.parametrize("nranks,axis", [(2, "z"), (4, "x"), (8, "y")])
+def test_virtual_slabs_spike_peer_ends(nranks, axis):
+    """Spike z-solve with the all-gather fused into k_zsub_ends (peer stores
+    into every rank's end-value buffer, etc_slab_set_ends_peers): bit for bit
+    the all-gather path (only the transport differs)."""
+    n = 64
+    f = P.gen_random_balls(n, 40, 0.05, 0.15, 100.0, 11)
+    cube = _canonical(f.kx.reshape(n, n, n), axis)
+    grid = (n, n, n, 1.0, 1.0, 1.0)
+    peer = dist.virtual_slab_solve(cube, grid, nranks, 1.0, 0.0, 1e-8, p2p=True, zsolve="spike")
+    base = dist.virtual_slab_solve(cube, grid, nranks, 1.0, 0.0, 1e-8, p2p=False, zsolve="spike")
+    for a, b in zip(peer, base):
+        assert a.iterations == b.iterations
+        assert a.relative_residuals == b.relative_residuals
+        assert a.kappa_eff == b.kappa_eff

@@ -27,7 +27,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank(rank, size, port, n, q, zsolve="pencil"):
+def _rank(rank, size, port, n, q, zsolve="pencil", p2p=True):
     try:
         sys.path.insert(0, str(ROOT))
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -46,7 +46,7 @@ def _rank(rank, size, port, n, q, zsolve="pencil"):
         ops = dist.CudaSlabOps(n, n, n, k0, nzl, size, rank, 1.0, 1.0, 1.0)
         comm = dist.TorchComm()
         rep = dist.slab_solve(ops, comm, k, k, k, (n, n, n, 1.0, 1.0, 1.0), 1.0, 0.0, 1e-8,
-                              p2p=zsolve == "pencil", zsolve=zsolve)
+                              p2p=p2p, zsolve=zsolve)
         q.put((rank, (rep.iterations, rep.kappa_eff, rep.relative_residuals,
                       ops.p2p_ok() or zsolve == "spike"), None))
         td.destroy_process_group()
@@ -56,10 +56,11 @@ def _rank(rank, size, port, n, q, zsolve="pencil"):
         q.put((rank, None, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("zsolve", ["pencil", "spike"])
-def test_two_processes_peer_exchange_over_ipc(zsolve):
+@pytest.mark.parametrize("zsolve,p2p", [("pencil", True), ("spike", False), ("spike", True)])
+def test_two_processes_peer_exchange_over_ipc(zsolve, p2p):
     """pencil: the peer-memory exchange over IPC; spike: the substructured
-    z-solve with its end values all-gathered by TorchComm (gloo)."""
+    z-solve with its end values all-gathered by TorchComm (gloo), or (p2p)
+    stored by k_zsub_ends into both ranks' IPC-opened end-value buffers."""
     import torch.multiprocessing as mp
 
     sys.path.insert(0, str(ROOT))
@@ -69,7 +70,7 @@ def test_two_processes_peer_exchange_over_ipc(zsolve):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, size, port, n, q, zsolve)) for r in range(size)]
+    procs = [ctx.Process(target=_rank, args=(r, size, port, n, q, zsolve, p2p)) for r in range(size)]
     for p in procs:
         p.start()
     res = []

@@ -100,7 +100,7 @@ class TorchComm:
             self.td.all_gather([host[r * n:(r + 1) * n] for r in range(self.size)], inp.cpu(), group=self.group)
             out.copy_(host)
             return
-        self.td.all_gather([out[r * n:(r + 1) * n] for r in range(self.size)], inp, group=self.group)
+        self.td.all_gather_into_tensor(out[:n * self.size], inp, group=self.group)
 
     def barrier(self):
         # peer stores were issued on the current stream: complete them first

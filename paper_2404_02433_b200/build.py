@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SRC = PKG / "csrc" / "etc_b200.cu"
-DEPS = [SRC, PKG / "csrc" / "etc_kernels.cuh", PKG / "csrc" / "etc_f32.cuh", ROOT / "include" / "etc_b200.h"]
+DEPS = [SRC, *sorted((PKG / "csrc").glob("*.cuh")), ROOT / "include" / "etc_b200.h"]
 LIB = PKG / "libetc_b200.so"
 
 NVCC_FLAGS = [

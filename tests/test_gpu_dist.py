@@ -53,7 +53,10 @@ def test_virtual_slabs_peer_exchange(nranks, axis):
     (etc_slab_set_peers): the forward transform stores into the destination
     ranks' pencil buffers, the z-solve into the owners' return buffers, halo
     planes go straight into the neighbours' halos.  Same solve as the NCCL
-    path (bit for bit: only the transport differs) and as one GPU."""
+    path and as one GPU.  The peer path's z-solve stores rows into the
+    owners' return buffers from k_thomas_x, the all-to-all path runs the
+    TMA-fed k_zsolve_tma: the same elimination bit for bit, with r.z summed
+    in another order, so histories agree to rounding."""
     n = 128
     f = P.gen_random_balls(n, 40, 0.05, 0.15, 100.0, 11)
     cube = _canonical(f.kx.reshape(n, n, n), axis)
@@ -67,8 +70,11 @@ def test_virtual_slabs_peer_exchange(nranks, axis):
     base = dist.virtual_slab_solve(cube, grid, nranks, 1.0, 0.0, 1e-8, p2p=False)
     for a, b in zip(peer, base):
         assert a.iterations == b.iterations
-        assert a.relative_residuals == b.relative_residuals
-        assert a.kappa_eff == b.kappa_eff
+        h, s = np.array(a.relative_residuals), np.array(b.relative_residuals)
+        big = s > 1e-2
+        assert np.all(np.abs(h[big] - s[big]) <= 1e-10 * s[big])
+        assert np.all(np.abs(h - s) <= 1e-1 * s)
+        assert abs(a.kappa_eff - b.kappa_eff) <= 1e-10 * abs(b.kappa_eff)
     single = P.homogenize(f, P.BoundaryConfig(P.Axis(axis), 1.0, 0.0), 1e-8)
     assert peer[0].iterations == single.iterations
     assert abs(peer[0].kappa_eff - single.kappa_eff) <= 1e-9 * abs(single.kappa_eff)

@@ -239,6 +239,75 @@ int etc_voxelize_fibres(double* out_dev, int n, const double* fibres_host, int c
 int etc_fill_channels(double* kx_dev, double* ky_dev, double* kz_dev, int cells_per_period, int periods,
                       double cx, double cy, double cz, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Operator-plugin layer (the reference's lower-level exports,
+ * __init__.py:9-71), used by paper_2404_02433_b200.plugin.
+ * ------------------------------------------------------------------------ */
+
+/* Geometry-only plan (no field): what FctPlan (transforms.py:56-61) and
+ * FctPreconditioner (preconditioner.py:273-282) need — etc_set_reference,
+ * then etc_dct2_xy / etc_dct3_xy / etc_thomas / etc_apply_precond (and the
+ * float32 variants below).  Field entry points fail with ETC_CONFIG. */
+int etc_plan_bare(etc_plan* plan);
+
+/* float32 transforms and preconditioner (FctPlan / FctPreconditioner with
+ * dtype=float32; the line passes of the f32 solve).  z != r. */
+int etc_dct2_xy_f32(etc_plan* plan, const float* in, float* out);
+int etc_dct3_xy_f32(etc_plan* plan, const float* in, float* out);
+int etc_apply_precond_f32(etc_plan* plan, const float* r, float* z);
+
+/* Stateless kernels on the reference's own data structures (etc_plugin.cu).
+ * prec: 0 float64, 1 float32 (every array of the call).  Arrays are device
+ * pointers; faces are a DiscreteSystem's compact arrays (tpfa.py:33-88):
+ * tx (nx-1)*ny*nz, ty nx*(ny-1)*nz, tz nx*ny*(nz-1), t_in / t_out nx*ny.
+ * Elementwise results follow numpy's operation order (bitwise). */
+const char* etc_op_last_error(void);
+/* doubles of device scratch the reductions below need for n elements */
+int etc_op_reduce_parts(long long n);
+/* apply_operator (tpfa.py:110-131) */
+int etc_op_stencil(int prec, int nx, int ny, int nz, const void* tx, const void* ty, const void* tz,
+                   const void* t_in, const void* t_out, const void* u, void* out, void* stream);
+/* operator_diagonal (tpfa.py:134-147) */
+int etc_op_diagonal(int prec, int nx, int ny, int nz, const void* tx, const void* ty, const void* tz,
+                    const void* t_in, const void* t_out, void* out, void* stream);
+/* build_system's faces from scale_field's cubes (tpfa.py:91-107) */
+int etc_op_faces(int prec, int nx, int ny, int nz, const void* sx, const void* sy, const void* sz, void* tx,
+                 void* ty, void* tz, void* t_in, void* t_out, void* stream);
+/* scale_field (tpfa.py:19-26): s = k / h2, h2 = dtype(h)**2 */
+int etc_op_scale(int prec, long long n, const void* k, double h2, void* s, void* stream);
+/* axis_permute of one cube (pipeline.py:87-111): axis 0 swapaxes(0,2), 1 swapaxes(0,1) */
+int etc_op_permute(int prec, int nx, int ny, int nz, int axis, const void* src, void* dst, void* stream);
+/* build_rhs (tpfa.py:150-167): p_in / p_out planes (ny*nx) or, when NULL, the scalars */
+int etc_op_rhs(int prec, int nx, int ny, int nz, const void* t_in, const void* t_out, const void* pin_plane,
+               double pin, const void* pout_plane, double pout, void* b, void* stream);
+/* reconstruct_boundary_flux (tpfa.py:234-251): side_out 1 "out", 0 "in" */
+int etc_op_flux(int prec, int nx, int ny, int nz, const void* t_layer, double hz, const void* u, double pval,
+                int side_out, void* out, void* stream);
+/* thomas_solve_batch (preconditioner.py:215-250), in place on x; upper:
+ * (nz-1)*ny*nx scratch; returns ETC_PIVOT with the first non-positive pivot's
+ * layer in *bad_layer (bad_dev: one device int of scratch) */
+int etc_op_thomas(int prec, int nx, int ny, int nz, const void* shift, const void* z_diag, double off, void* x,
+                  void* upper, int* bad_dev, int* bad_layer, void* stream);
+/* kind 0: out = a*b, 1: out = 1/a, 2: out = a+b */
+int etc_op_elementwise(int prec, int kind, long long n, const void* a, const void* b, void* out, void* stream);
+/* deterministic float64 reductions into out (device): kind 0 a.b, 1 (a.b, a.a, b.b), 2 sum(a) */
+int etc_op_dots(int prec, int kind, long long n, const void* a, const void* b, double* parts, double* out,
+                void* stream);
+/* pcg's update (krylov.py:76-77): p += alpha w; r -= alpha z; *rr_out (device) = r.r */
+int etc_op_pcg_update(int prec, long long n, double alpha, void* p, const void* w, void* r, const void* z,
+                      double* parts, double* rr_out, void* stream);
+/* w = z + beta w (krylov.py:89) */
+int etc_op_xpby(int prec, long long n, const void* z, double beta, void* w, void* stream);
+/* exact (min, max) of a positive array into out (host; mm: 2 device uint64) */
+int etc_op_minmax(int prec, long long n, const void* a, void* mm, double out[2], void* stream);
+/* SsorPreconditioner apply (preconditioner.py:285-321), float64: the two
+ * triangular sweeps of the stencil in natural order, level-scheduled */
+int etc_op_ssor(int nx, int ny, int nz, const double* tx, const double* ty, const double* tz, const double* diag,
+                double omega, const double* r, double* out, void* stream);
+/* assemble_dense (tpfa.py:181-205), float64, n = nx*ny*nz <= 4096: mat n*n */
+int etc_op_dense(int nx, int ny, int nz, const double* tx, const double* ty, const double* tz,
+                 const double* t_in, const double* t_out, double* mat, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

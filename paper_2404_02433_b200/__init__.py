@@ -45,5 +45,43 @@ from .solver import (
 )
 from .operators import DeviceSystem
 from ._native import NativeUnavailable
+# the reference's operator-plugin layer under its own names (plugin.py;
+# reference __init__.py:9-71)
+from .plugin import (
+    DiscreteSystem,
+    FctPlan,
+    FctPreconditioner,
+    JacobiPreconditioner,
+    SlabBuffer,
+    TridiagFactors,
+    add_source,
+    apply_operator,
+    assemble_dense,
+    axis_permute,
+    build_rhs,
+    build_system,
+    build_tridiag,
+    coefficient_stats,
+    condition_estimate,
+    dct1d_ref_backward,
+    dct1d_ref_forward,
+    dense_solve,
+    effective_conductivity,
+    fct_backward_batch,
+    fct_forward_batch,
+    fct_pre_permute,
+    fct_precond_apply,
+    identity_apply,
+    jacobi_apply,
+    l2_error_midpoint,
+    operator_diagonal,
+    pcg,
+    reconstruct_boundary_flux,
+    reference_system,
+    scale_field,
+    ssor_apply,
+    thomas_solve_batch,
+)
+from .grid import gen_smooth_problem
 
 __version__ = "0.1.0"

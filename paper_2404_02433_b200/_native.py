@@ -27,6 +27,10 @@ EXPORTS = (
     "etc_voxelize_balls", "etc_voxelize_fibres", "etc_fill_channels", "etc_slab_create", "etc_slab_load", "etc_slab_plane",
     "etc_slab_init", "etc_slab_run", "etc_slab_status", "etc_slab_fused", "etc_slab_p2p_ok", "etc_slab_xbuf",
     "etc_slab_set_peers", "etc_slab_set_ends_peers", "etc_slab_plane_ptr", "etc_ipc_handle", "etc_ipc_open", "etc_ipc_close",
+    "etc_plan_bare", "etc_dct2_xy_f32", "etc_dct3_xy_f32", "etc_apply_precond_f32",
+    "etc_op_last_error", "etc_op_reduce_parts", "etc_op_stencil", "etc_op_diagonal", "etc_op_faces", "etc_op_scale",
+    "etc_op_permute", "etc_op_rhs", "etc_op_flux", "etc_op_thomas", "etc_op_elementwise", "etc_op_dots",
+    "etc_op_pcg_update", "etc_op_xpby", "etc_op_minmax", "etc_op_dense", "etc_op_ssor",
 )
 
 
@@ -56,6 +60,7 @@ _P = C.c_void_p
 _D = C.c_double
 _I = C.c_int
 _DP = C.POINTER(C.c_double)
+_L = C.c_longlong
 
 _SIGS = {
     "etc_last_error": (C.c_char_p, []),
@@ -98,6 +103,27 @@ _SIGS = {
     "etc_ipc_handle": (_I, [_P, _P, _P, C.POINTER(C.c_size_t)]),
     "etc_ipc_open": (_I, [_P, C.POINTER(_P)]),
     "etc_ipc_close": (_I, [_P]),
+    "etc_plan_bare": (_I, [_P]),
+    "etc_dct2_xy_f32": (_I, [_P, _P, _P]),
+    "etc_dct3_xy_f32": (_I, [_P, _P, _P]),
+    "etc_apply_precond_f32": (_I, [_P, _P, _P]),
+    "etc_op_last_error": (C.c_char_p, []),
+    "etc_op_reduce_parts": (_I, [_L]),
+    "etc_op_stencil": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "etc_op_diagonal": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "etc_op_faces": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "etc_op_scale": (_I, [_I, _L, _P, _D, _P, _P]),
+    "etc_op_permute": (_I, [_I, _I, _I, _I, _I, _P, _P, _P]),
+    "etc_op_rhs": (_I, [_I, _I, _I, _I, _P, _P, _P, _D, _P, _D, _P, _P]),
+    "etc_op_flux": (_I, [_I, _I, _I, _I, _P, _D, _P, _D, _I, _P, _P]),
+    "etc_op_thomas": (_I, [_I, _I, _I, _I, _P, _P, _D, _P, _P, _P, C.POINTER(_I), _P]),
+    "etc_op_elementwise": (_I, [_I, _I, _L, _P, _P, _P, _P]),
+    "etc_op_dots": (_I, [_I, _I, _L, _P, _P, _P, _P, _P]),
+    "etc_op_pcg_update": (_I, [_I, _L, _D, _P, _P, _P, _P, _P, _P, _P]),
+    "etc_op_xpby": (_I, [_I, _L, _P, _D, _P, _P]),
+    "etc_op_minmax": (_I, [_I, _L, _P, _P, _DP, _P]),
+    "etc_op_dense": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "etc_op_ssor": (_I, [_I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P]),
 }
 
 

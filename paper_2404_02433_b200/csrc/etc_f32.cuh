@@ -736,3 +736,35 @@ extern "C" int etc_set_precision(etc_plan* pl, int bits) {
   pl->prec32 = bits == 32;
   return ETC_OK;
 }
+
+// ---- float32 operator-plugin entry points (the reference's FctPlan /
+// FctPreconditioner with dtype=float32, transforms.py:56-61 and
+// preconditioner.py:273-282): the same line passes and elimination as the
+// f32 solve, on caller vectors.  Need etc_set_reference (field or bare plan).
+static int f32_tabs_ready(etc_plan* pl) {
+  if (!pl || !pl->have_axis) return fail(ETC_CONFIG, "select an axis first");
+  if (!pl->have_ref) return fail(ETC_CONFIG, "set the reference first");
+  if (pl->slab) return fail(ETC_CONFIG, "precision f32 runs on single-GPU plans");
+  return f32_set_reference(pl);
+}
+
+extern "C" int etc_dct2_xy_f32(etc_plan* pl, const float* in, float* out) {
+  int rc;
+  if ((rc = f32_tabs_ready(pl))) return rc;
+  if ((rc = f32_pass<0, 0>(pl, in, out, 0))) return rc;
+  return f32_pass<1, 0>(pl, out, out, 0);
+}
+
+extern "C" int etc_dct3_xy_f32(etc_plan* pl, const float* in, float* out) {
+  int rc;
+  if ((rc = f32_tabs_ready(pl))) return rc;
+  if ((rc = f32_pass<1, 1>(pl, in, out, 0))) return rc;
+  return f32_pass<0, 1>(pl, out, out, 0);
+}
+
+extern "C" int etc_apply_precond_f32(etc_plan* pl, const float* r, float* z) {
+  int rc;
+  if ((rc = f32_tabs_ready(pl))) return rc;
+  if (r == z) return fail(ETC_CONFIG, "etc_apply_precond_f32 needs distinct input and output");
+  return f32_precond(pl, r, pl->v32[5], z, 0);
+}

@@ -77,6 +77,14 @@ class GridSpec:
     def n_cells(self) -> int:
         return self.nx * self.ny * self.nz
 
+    def cell_centers(self):
+        """Coordinate arrays (X, Y, Z), each shaped (nz, ny, nx) (grid.py:84-90)."""
+        cx = (np.arange(self.nx) + 0.5) * self.hx
+        cy = (np.arange(self.ny) + 0.5) * self.hy
+        cz = (np.arange(self.nz) + 0.5) * self.hz
+        Z, Y, X = np.meshgrid(cz, cy, cx, indexing="ij")
+        return X, Y, Z
+
 
 def linear_index(i: int, j: int, k: int, grid: GridSpec) -> int:
     """x-fastest flat offset (reference grid.py:93-99)."""
@@ -109,8 +117,8 @@ class OrthotropicField:
                 continue
             if _is_tensor(arr):
                 a = arr.reshape(-1)
-                if a.dtype.__str__() != "torch.float64":
-                    raise ConfigError(f"{name}: CUDA fields must be float64")
+                if a.dtype.__str__() not in ("torch.float64", "torch.float32"):
+                    raise ConfigError(f"{name}: CUDA fields must be float64 or float32")
                 if not a.is_contiguous():
                     a = a.contiguous()
                 if a.numel() != grid.n_cells:
@@ -150,6 +158,29 @@ class OrthotropicField:
 
     def cube(self, component: str):
         return getattr(self, component).reshape(self.grid.shape)
+
+    def astype(self, dtype) -> "OrthotropicField":
+        """The field cast to float32 / float64 (grid.py:139-148)."""
+        dtype = np.dtype(dtype)
+        if dtype == np.dtype(str(self.dtype).replace("torch.", "")):
+            return self
+        if self.on_device:
+            import torch
+
+            td = torch.float32 if dtype == np.float32 else torch.float64
+            return OrthotropicField(self.grid, self.kx.to(td), self.ky.to(td), self.kz.to(td), validate=False)
+        return OrthotropicField(self.grid, self.kx.astype(dtype), self.ky.astype(dtype), self.kz.astype(dtype))
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, OrthotropicField) or other.grid != self.grid:
+            return False
+
+        def host(a):
+            return a.cpu().numpy() if _is_tensor(a) else a
+
+        return all(np.array_equal(host(getattr(self, c)), host(getattr(other, c))) for c in ("kx", "ky", "kz"))
+
+    __hash__ = None
 
 
 @dataclass(frozen=True)
@@ -231,6 +262,30 @@ def gen_center_ball(n: int, kappa_inc: float, device=None, as_numpy: bool = Fals
     if kappa_inc <= 0.0:
         raise ConfigError("kappa_inc must be positive")
     return _voxelize(n, np.array([[0.5, 0.5, 0.5, 0.25]]), kappa_inc, device, as_numpy)
+
+
+def gen_smooth_problem(n: int):
+    """Smooth manufactured problem on the unit cube (reference grid.py:182-227):
+    K = Diag(cos(pi y) + 2, 2 e^z, 3 cos(pi x) + 4) at cell centres, exact
+    p = cos(pi x) cos(pi y) e^z and its source f = -div(K grad p).  Returns
+    (field, exact, source); the field is host data (a verification input, not
+    a benchmark one), the two samplers are vectorised numpy callables."""
+    if n < 2:
+        raise ConfigError("smooth problem needs n >= 2")
+    grid = GridSpec(n, n, n)
+    X, Y, Z = grid.cell_centers()
+    field = OrthotropicField(grid, np.cos(np.pi * Y) + 2.0, 2.0 * np.exp(Z), 3.0 * np.cos(np.pi * X) + 4.0)
+
+    def exact(x, y, z):
+        return np.cos(np.pi * x) * np.cos(np.pi * y) * np.exp(z)
+
+    def source(x, y, z):
+        cc = np.cos(np.pi * x) * np.cos(np.pi * y)
+        return (np.pi ** 2 * (np.cos(np.pi * y) + 2.0) * cc * np.exp(z)
+                + 2.0 * np.pi ** 2 * cc * np.exp(2.0 * z)
+                - (3.0 * np.cos(np.pi * x) + 4.0) * cc * np.exp(z))
+
+    return field, exact, source
 
 
 # ----------------------------------------------------------------------------

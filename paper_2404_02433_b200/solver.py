@@ -139,6 +139,8 @@ class DevicePlan:
             if on_dev:
                 if a.device != self.device:
                     a = a.to(self.device)
+                if a.dtype != torch.float64:  # float32 fields widen exactly (the f32 solve casts back)
+                    a = a.to(torch.float64)
                 keep.append(a)
                 ptrs.append(a.data_ptr())
             else:
@@ -150,7 +152,11 @@ class DevicePlan:
         with torch.cuda.device(self.device):
             _check(self.lib.etc_load_field(self._h, ptrs[0], ptrs[1], ptrs[2], 1 if on_dev else 0),
                    "etc_load_field")
-        self._keepalive = keep  # host buffers must outlive the async copy
+        # host buffers must outlive the async copy; the keyed objects
+        # themselves are kept too, so their ids cannot be reused by another
+        # field while this key is current (a converted copy alone would not
+        # pin them)
+        self._keepalive = (fld, arrs, keep)
         self._field_key = key
         self.axis = None
 
@@ -298,8 +304,10 @@ def _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_
         raise ConfigError(f"ref mode must be opt or one, got {ref_mode!r}")
     kind, omega = _parse_precond(precond, omega)
     if kind == "ssor":
-        raise ConfigError("ssor (SciPy SuperLU triangular sweeps) is not implemented on the device; "
-                          "use fct, jacobi or none")
+        if keep_solution:
+            raise ConfigError("the full-solution mode runs the fused preconditioners (fct | jacobi | none)")
+        return _homogenize_composed(field, boundary, rtol, kind, ref_mode, precision, omega, max_iter,
+                                    device), None
     if precision == "f32" and kind == "jacobi":
         raise ConfigError("precision f32 runs with the fct and none preconditioners")
     if precision == "f32" and keep_solution:
@@ -340,6 +348,52 @@ def _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_
         device_ms=float(info.device_ms),
     )
     return rep, sol
+
+
+def _homogenize_composed(field, boundary, rtol, kind, ref_mode, precision, omega, max_iter, device):
+    """homogenize() composed from the operator-plugin layer, statement for
+    statement the reference pipeline (pipeline.py:153-175): permute, build,
+    stats, LP, preconditioner, rhs, pcg over device tensors, flux, kappa.
+    Used for the preconditioners the fused solve does not carry (ssor)."""
+    from . import plugin
+
+    if rtol <= 0.0:
+        raise ValueError("rtol must be positive")
+    if max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+    fld = _as_field(field)
+    torch = _torch()
+    dev = torch.device(device) if device is not None else (fld.kx.device if fld.on_device else
+                                                           torch.device("cuda", torch.cuda.current_device()))
+    with torch.cuda.device(dev):
+        t0 = time.perf_counter()
+        dt = np.float32 if precision == "f32" else np.float64
+        arrs = [plugin._to_dev(a, dt) for a in (fld.kx, fld.ky, fld.kz)]
+        work = plugin.axis_permute(OrthotropicField(fld.grid, *arrs, validate=False), boundary.axis)
+        canon = BoundaryConfig(Axis.Z, boundary.p_in, boundary.p_out)
+        sys = plugin.build_system(work, canon)
+        stats = plugin.coefficient_stats(sys)
+        refs = solve_reference_lp(stats) if ref_mode == "opt" else ones_reference(stats)
+        if kind == "ssor":
+            apply_m = plugin.SsorPreconditioner(sys, omega)
+        elif kind == "fct":
+            apply_m = plugin.FctPreconditioner(sys.grid, refs, dt)
+        elif kind == "jacobi":
+            apply_m = plugin.JacobiPreconditioner(sys)
+        else:
+            apply_m = plugin.identity_apply
+        b = plugin.build_rhs(sys)
+        prep = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        solution, report = plugin.pcg(lambda u: plugin.apply_operator(sys, u), apply_m, b, rtol, max_iter)
+        flux = plugin.reconstruct_boundary_flux(sys, solution)
+        report.kappa_eff = plugin.effective_conductivity(sys, flux)
+        report.exec_seconds = time.perf_counter() - t1
+    report.prep_seconds = prep
+    report.precision = precision
+    report.preconditioner = f"ssor:{omega:g}" if kind == "ssor" else kind
+    report.ref_params = refs
+    return report
 
 
 def effective_tensor(field, rtol: float = 1e-9, p_in: float = 1.0, p_out: float = 0.0,

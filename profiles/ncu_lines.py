@@ -7,7 +7,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+kf = sys.argv[3:4]
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"] + (["-k", "regex:" + kf[0]] if kf else []),
                      capture_output=True, text=True).stdout
 rows, path, hdr = [], "?", None
 for r in csv.reader(io.StringIO(out)):

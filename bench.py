@@ -501,7 +501,15 @@ def main():
     ap.add_argument("--zsolve", choices=["pencil", "spike"], default=None,
                     help="z-slab z-solve: pencil all-to-alls, or the substructured spike solve (default for N > 1)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun (the driver launches it that way itself)
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                                   "--master-port", os.environ.get("MASTER_PORT", "29512"), __file__,
+                                   *sys.argv[1:]])
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}: launch one process per GPU")
     if args.zsolve is None:
         args.zsolve = "spike" if world > 1 else "pencil"
     rank = int(os.environ.get("RANK", "0"))

@@ -108,6 +108,13 @@ class TorchComm:
         _torch().cuda.current_stream().synchronize()
         self.td.barrier(group=self.group)
 
+    def peer_access_ok(self) -> bool:
+        """Whether this rank's device can map every other visible device's
+        memory (the precondition of the peer-store paths)."""
+        torch = _torch()
+        me, n = torch.cuda.current_device(), torch.cuda.device_count()
+        return all(torch.cuda.can_device_access_peer(me, d) for d in range(n) if d != me)
+
     def share_pointers(self, ops, ptrs):
         """Every rank's device pointers `ptrs` as pointers valid in this
         process: own ones as they are, the peers' opened through CUDA IPC
@@ -154,6 +161,15 @@ def _ipc_open(handle: bytes, offset: int) -> int:
         _check(_native.lib().etc_ipc_open(C.c_char_p(handle), C.byref(ptr)), "etc_ipc_open")
         base = _IPC_OPEN[handle] = int(ptr.value)
     return base + offset
+
+
+def release_ipc() -> None:
+    """Close every peer allocation this process opened (they pin the peers'
+    memory); call when the plans that used them are released."""
+    lib = _native.lib()
+    for base in _IPC_OPEN.values():
+        lib.etc_ipc_close(C.c_void_p(base))
+    _IPC_OPEN.clear()
 
 
 class _ThreadHub:
@@ -322,10 +338,18 @@ class CudaSlabOps:
         return bytes(buf.raw), int(off.value)
 
     def set_ends_peers(self, ptrs):
+        """Peer end-value buffers for k_zsub_ends (None: back to the all-gather)."""
+        if ptrs is None:
+            _check(self.lib.etc_slab_set_ends_peers(self._h, None), "etc_slab_set_ends_peers")
+            return
         arr = C.c_void_p * len(ptrs)
         _check(self.lib.etc_slab_set_ends_peers(self._h, arr(*ptrs)), "etc_slab_set_ends_peers")
 
     def set_peers(self, recv_ptrs, back_ptrs):
+        """Peer pencil / return buffers (None: the all-to-all path)."""
+        if recv_ptrs is None or back_ptrs is None:
+            _check(self.lib.etc_slab_set_peers(self._h, None, None), "etc_slab_set_peers")
+            return
         arr = C.c_void_p * len(recv_ptrs)
         _check(self.lib.etc_slab_set_peers(self._h, arr(*recv_ptrs), arr(*back_ptrs)), "etc_slab_set_peers")
 
@@ -402,6 +426,11 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
             p2p = os.environ.get("ETC_P2P", "0") == "1"
         # the end values go to the peers by stores from k_zsub_ends (no all-gather)
         spike_p2p = bool(p2p) and hasattr(comm, "share_pointers") and hasattr(ops, "set_ends_peers")
+        if p2p and comm.size > 1:  # every rank must agree (else the collectives mismatch and hang)
+            t = ops.new(1)
+            t.fill_(float(spike_p2p and getattr(comm, "peer_access_ok", lambda: True)()))
+            comm.allreduce(t, "min")
+            spike_p2p = bool(float(t.cpu().item()) > 0.5)
         p2p = False
     iso = kx is ky and ky is kz
     ops.load(kx, ky, kz)
@@ -415,6 +444,13 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
         t.fill_(float(use_p2p))
         comm.allreduce(t, "min")
         use_p2p = bool(float(t.cpu().item()) > 0.5)
+    # plans are cached across solves: peer tables a previous solve installed
+    # must not leak into this one's mode (the kernels would store into the
+    # peers' buffers and skip the local ones)
+    if not use_p2p and hasattr(ops, "set_peers"):
+        ops.set_peers(None, None)
+    if not spike_p2p and hasattr(ops, "set_ends_peers"):
+        ops.set_ends_peers(None)
     if use_p2p:
         # [pencil, return, s_x, s_y, s_z, w] (plane 0) of every rank
         table = comm.share_pointers(ops, [ops.xbuf(0), ops.xbuf(1), ops.plane_ptr(0, 0), ops.plane_ptr(1, 0),
@@ -586,6 +622,12 @@ def virtual_slab_solve(field_cube, grid, nranks: int, p_in=1.0, p_out=0.0, rtol=
 # ----------------------------------------------------------------------------
 
 _OPS_CACHE: dict = {}
+
+
+def release_slab_plans() -> None:
+    """Drop the cached rank plans and close the peer allocations they opened."""
+    _OPS_CACHE.clear()
+    release_ipc()
 
 
 def _canonical(fld, axis: str):

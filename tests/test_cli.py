@@ -63,8 +63,10 @@ def test_solve_matches_reference_cli(tmp_path):
     w = np.array([float(r["relres"]) for r in csv.DictReader(open(GOLD / "cli_ball8_history.csv"))])
     big = w > 1e-2  # 1e-8 while relres > 1e-2
     assert len(h) == len(w) and np.all(np.abs(h[big] - w[big]) <= 1e-8 * w[big])
-    # a configuration error (SSOR has no device path) maps to exit 2
-    assert main(["solve", str(GOLD / "ball8.vox"), "--precond", "ssor"]) == 2
+    # SSOR runs through the plugin composition (exit 0); a configuration
+    # error maps to exit 2 (cli.py:309-323)
+    assert main(["solve", str(GOLD / "ball8.vox"), "--precond", "ssor", "--omega", "1.2"]) == 0
+    assert main(["solve", str(GOLD / "ball8.vox"), "--precond", "ssor", "--omega", "2.5"]) == 2
 
 
 @pytest.mark.gpu

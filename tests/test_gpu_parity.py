@@ -405,10 +405,29 @@ def test_jacobi_diagonal_and_first_iteration_bitwise():
     assert abs(rep.relative_residuals[1] - ref["history"][1]) <= 1e-13 * ref["history"][1]
 
 
-def test_ssor_is_a_config_error():
+def test_ssor_against_reference_runs():
+    """precond="ssor[:omega]" (pipeline.py:114-132): the device SSOR sweeps
+    (level-scheduled triangular solves, etc_op_ssor) under the plugin pcg,
+    against the reference's SuperLU-based runs (tests/golden/solves_ssor.json):
+    iterations within 1, kappa within 1e-8 (1e-7 at contrast 1000), history
+    within 1e-8 while relres > 1e-2; a bad omega is a ConfigError."""
+    import json
+
+    runs = json.loads((Path(__file__).resolve().parent / "golden" / "solves_ssor.json").read_text())
+    for c in runs:
+        f = P.gen_random_balls(c["n"], 40, 0.05, 0.15, c["kappa"], 11)
+        rep = P.homogenize(f, P.BoundaryConfig(P.Axis(c["axis"]), 1.0, 0.0), c["rtol"], precond=c["precond"])
+        assert rep.preconditioner == c["preconditioner"]
+        assert abs(rep.iterations - c["iterations"]) <= 1, (c, rep.iterations)
+        tol = 1e-7 if c["kappa"] >= 1000 else 1e-8
+        assert abs(rep.kappa_eff - c["kappa_eff"]) <= tol * c["kappa_eff"], (c, rep.kappa_eff)
+        h, w = np.array(rep.relative_residuals), np.array(c["history"])
+        m = min(len(h), len(w))
+        big = w[:m] > 1e-2
+        assert np.all(np.abs(h[:m][big] - w[:m][big]) <= 1e-8 * w[:m][big])
     f = P.gen_random_balls(8, 40, 0.05, 0.15, 10.0, 11)
     with pytest.raises(P.ConfigError):
-        P.homogenize(f, P.BoundaryConfig(P.Axis("z"), 1.0, 0.0), 1e-6, precond="ssor:1.2")
+        P.homogenize(f, P.BoundaryConfig(P.Axis("z"), 1.0, 0.0), 1e-6, precond="ssor:2.2")
 
 
 def test_channels_generator_and_solves(golden_channels):

@@ -246,6 +246,28 @@ def precond(tab, r: np.ndarray, workers: int = 0, reverse: bool = False) -> np.n
     return fct_backward(solve(shift, zd, off, fct_forward(r, workers)), workers)
 
 
+def _dct_tables(n: int):
+    i = np.arange(n)
+    fwd = np.cos(np.pi * (2 * i[None, :] + 1) * i[:, None] / (2 * n))  # uh = C u (transforms.py:9-15)
+    w = np.where(i == 0, 0.5, 1.0)
+    bwd = (2.0 / n) * np.cos(np.pi * (2 * i[:, None] + 1) * i[None, :] / (2 * n)) * w[None, :]
+    return fwd, bwd
+
+
+def precond_matmul(tab, r: np.ndarray) -> np.ndarray:
+    """z = B T F r with the cosine transforms as dense matrix products (the
+    direct sums of transforms.py:24-38, BLAS-ordered): a third valid
+    rounding of the same preconditioner, independent of any FFT, used to
+    measure the implementation spread at contrast 1000."""
+    _, _, shift, zd, off = tab
+    nz, ny, nx = r.shape
+    fx, bx = _dct_tables(nx)
+    fy, by = _dct_tables(ny)
+    t = np.einsum("pj,kjq->kpq", fy, np.einsum("qi,kji->kjq", fx, r, optimize=True), optimize=True)
+    t = thomas(shift, zd, off, t)
+    return np.einsum("jp,kpi->kji", by, np.einsum("iq,kpq->kpi", bx, t, optimize=True), optimize=True)
+
+
 # ----------------------------------------------------------------------------
 # PCG (reference krylov.py:36-91, Alg. 1)
 # ----------------------------------------------------------------------------
@@ -357,10 +379,12 @@ def jacobi_inverse_diagonal(fc, shape) -> np.ndarray:
 
 def homogenize(kx, ky, kz, grid, axis="z", p_in=1.0, p_out=0.0, rtol=1e-9,
                ref_mode="opt", max_iter=1024, workers: int = 0, perturbed: bool = False,
-               precond: str = "fct") -> dict:
+               precond: str = "fct", dct: str = "fft") -> dict:
     """kx, ky, kz: (nz, ny, nx) cubes; grid = (nx, ny, nz, lx, ly, lz).
     perturbed=True: reversed stencil association, bottom-up z elimination and
     exactly rounded dots (same algorithm, different rounding).
+    dct="matmul": the preconditioner's cosine transforms as dense matrix
+    products instead of FFTs (precond_matmul).
     precond: "fct" (the FCT preconditioner), "jacobi" (r * 1/diag(A),
     preconditioner.py:324-330) or "none" (a copy of r, :337-338), selected as
     pipeline.py:114-132 does."""
@@ -374,7 +398,9 @@ def homogenize(kx, ky, kz, grid, axis="z", p_in=1.0, p_out=0.0, rtol=1e-9,
     tab = tables(nx, ny, nz, refs, kx.dtype.type)
     b = rhs(fc, kx.shape, p_in, p_out).reshape(-1)
     shape = kx.shape
-    if precond == "fct":
+    if precond == "fct" and dct == "matmul":
+        apply_m = lambda r: precond_matmul(tab, r.reshape(shape)).reshape(-1)  # noqa: E731
+    elif precond == "fct":
         apply_m = lambda r: precond_fct(tab, r.reshape(shape), workers, perturbed).reshape(-1)  # noqa: E731
     elif precond == "jacobi":
         invd = jacobi_inverse_diagonal(fc, shape).reshape(-1)

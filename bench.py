@@ -36,6 +36,15 @@ def cfg_tag(args) -> str:
     return " (BASELINE config 4)" if (args.n, args.contrast) == (512, 100.0) else ""
 
 
+def bench_config(args) -> dict:
+    """The workload both arms report (identical keys and values)."""
+    n = args.n
+    return {"workload": f"{n}^3 random-inclusion RVE, contrast {args.contrast:g}, directions {args.axes}, "
+                        f"rtol {args.rtol:g}, f64{cfg_tag(args)}",
+            "n": n, "contrast": args.contrast, "rtol": args.rtol, "directions": args.axes,
+            "l2": "inputs larger than L2 (one f64 vector = %.2f GB)" % (8 * n ** 3 / 1e9)}
+
+
 def metric_for(args) -> str:
     """BASELINE.json's metric for the default workload; the same wording with
     the actual size / contrast / directions / rtol otherwise."""
@@ -340,15 +349,6 @@ def run_b200(args, rank, world, local_rank):
         "iteration_frac": round(sum(kern[k]["bytes_per_launch"] * kern[k]["launches"] for k in it_kernels) / 1e9
                                 / (sum(kern[k]["ms_total"] for k in it_kernels) * 1e-3) / peaks["hbm_gbs"], 4),
     }
-    if "stencil" in kern:
-        # SURVEY 8(d)'s accounting: 160 B/cell per iteration for the minimal
-        # unfused pass structure; the fused kernels move 89, so this effective
-        # fraction is what the iteration achieves against that budget
-        its = kern["stencil"]["launches"]
-        roofline["survey_bytes_per_cell"] = 160
-        roofline["survey_effective_frac"] = round(160 * N * its / 1e9 / (sum(kern[k]["ms_total"] for k in it_kernels)
-                                                                        * 1e-3) / peaks["hbm_gbs"], 4)
-
     # end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -360,7 +360,7 @@ def run_b200(args, rank, world, local_rank):
         hostgrid = field.grid
         torch.cuda.synchronize()
         t_e2e = []
-        for it in range(max(1, min(args.steps, 3)) + 1):
+        for it in range(args.steps + 1):
             hf = P.OrthotropicField(hostgrid, kh, kh, kh, validate=False)  # fresh object: re-uploaded
             torch.cuda.synchronize()
             if dist:
@@ -373,7 +373,7 @@ def run_b200(args, rank, world, local_rank):
             if it > 0:  # first call is a warm-up
                 t_e2e.append(time.perf_counter() - t0)
         e2e = {"value": round(statistics.mean(t_e2e), 4), "unit": "s",
-               "h2d_bytes_per_step": int(kh.nbytes if not dist else 3 * kh.nbytes // world),
+               "h2d_bytes_per_step": int(kh.nbytes if not dist else kh.nbytes // world),  # dist: this rank's slab
                "d2h_bytes_per_step": int(sum(8 * (r.iterations + 1) + 8 for r in rp.values())),
                "samples": len(t_e2e),
                "api": "paper_2404_02433_b200.effective_tensor(numpy field in pinned host memory)"}
@@ -395,16 +395,13 @@ def run_b200(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: random-ball RVE (preset a: 40 balls r 0.05-0.15, seed 11), voxelised on device",
-        "config": {
-            "workload": f"{n}^3 random-inclusion RVE, contrast {args.contrast:g}, directions {axes}, "
-                        f"rtol {args.rtol:g}, f64{cfg_tag(args)}",
-            "n": n, "contrast": args.contrast, "rtol": args.rtol, "directions": axes,
+        "config": bench_config(args),
+        "details": {
             "iterations": iters, "ms_per_iter": round(ms_step / max(1, total_iters), 4),
             "kappa_eff": {a: reps[a].kappa_eff for a in axes},
             "parallelism": (f"z-slab x{world} (NCCL halo + pencil all-to-all + all-reduce)" if args.zsolve == "pencil"
                             else f"z-slab x{world} (NCCL halo + spike z-solve all-gather + all-reduce)") if dist
                            else "single",
-            "l2": "inputs larger than L2 (one f64 vector = %.2f GB)" % (8 * N / 1e9),
         },
         "roofline": roofline, "kernels": kern, "e2e": e2e, "cpu_baseline": cpu,
         "gpu_launches": launches, "clocks": clk,
@@ -472,10 +469,9 @@ def run_reference(args, rank, world):
         "warmup": args.warmup, "ms_per_step": round(it_s * 1e3, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic: random-ball RVE (preset a), host voxeliser",
         "impl": "reference",
-        "config": {"workload": f"{n}^3 random-inclusion RVE, contrast {args.contrast:g}, directions {args.axes}, "
-                               f"rtol {args.rtol:g}, f64{cfg_tag(args)}",
-                   "n": n, "iterations": iters, "setup_s": round(t_setup, 3), "iter_s": round(it_s, 4),
-                   "iterations_source": "tests/golden/solves_512.json (reference runs); 48 where absent"},
+        "config": bench_config(args),
+        "details": {"iterations": iters, "setup_s": round(t_setup, 3), "iter_s": round(it_s, 4),
+                    "iterations_source": "tests/golden/solves_512.json (reference runs); 48 where absent"},
         "cpu_baseline": {"value": round(value, 3), "unit": "s", "cores": workers, "kind": "port",
                          "sample": f"one PCG iteration of the oracle port per step at {n}^3 ({workers} FFT workers, "
                                    f"numpy ufuncs 1 core); value = {len(args.axes)} setups + {total} iterations"},

@@ -353,6 +353,24 @@ class CudaSlabOps:
         arr = C.c_void_p * len(recv_ptrs)
         _check(self.lib.etc_slab_set_peers(self._h, arr(*recv_ptrs), arr(*back_ptrs)), "etc_slab_set_peers")
 
+    def plane_view(self, which: int, plane: int):
+        """A zero-copy float64 tensor over one plane of the plan's buffer
+        `which` (planes -1 and nzl are the halos): collectives read and
+        write the plan's planes in place, no staging copies."""
+        key = (which, plane)
+        views = self.__dict__.setdefault("_views", {})
+        if key not in views:
+            torch = _torch()
+            ptr = self.plane_ptr(which, plane)
+            n = self.nx * self.ny
+
+            class _Plane:  # __cuda_array_interface__ carrier (the memory is the plan's)
+                __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                            "strides": None}
+
+            views[key] = torch.as_tensor(_Plane(), device=self.device)
+        return views[key]
+
     def put_plane(self, which: int, plane: int, dst_ptr: int):
         """Copy this rank's plane into a (peer) device address."""
         _check(self.lib.etc_slab_plane(self._h, which, plane, C.c_void_p(dst_ptr), 1), "etc_slab_plane")
@@ -378,6 +396,15 @@ class SlabResult:
 
 
 def _exchange_planes(ops, comm, which: int, nzl: int):
+    """One halo plane each way: my first plane -> the lower neighbour's upper
+    halo, my last plane -> the upper neighbour's lower halo, sent and
+    received in place through views of the plan's planes."""
+    if comm.size == 1:
+        return
+    if hasattr(ops, "plane_view"):
+        comm.neighbours(ops.plane_view(which, 0), ops.plane_view(which, nzl - 1), ops.plane_view(which, -1),
+                        ops.plane_view(which, nzl))
+        return
     lo = ops.get_plane(which, 0)
     hi = ops.get_plane(which, nzl - 1)
     recv_lo = ops.new(lo.numel())
@@ -389,8 +416,24 @@ def _exchange_planes(ops, comm, which: int, nzl: int):
         ops.set_plane(which, nzl, recv_hi)
 
 
+def _next_check(it: int, history: list, rtol: float, cap: int = 16) -> int:
+    """Iteration of the next host status read.  The device stops itself
+    (Ctl.done; every stage kernel early-exits), so the host only needs to
+    notice: predict the iteration that reaches rtol from the recent
+    geometric residual rate and look again there (at most `cap` later)."""
+    h = [v for v in history if v > 0.0]
+    if len(h) < 3 or h[-1] <= rtol:
+        return it + 1
+    span = min(len(h) - 1, 8)
+    rate = (h[-1] / h[-1 - span]) ** (1.0 / span)
+    if not (0.0 < rate < 1.0):
+        return it + 4
+    need = np.log(rtol / h[-1]) / np.log(rate)
+    return it + int(max(1, min(cap, np.floor(need))))
+
+
 def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_mode="opt",
-               max_iter=1024, check_every=1, p2p=None, zsolve=None) -> SolveReport:
+               max_iter=1024, check_every=None, p2p=None, zsolve=None) -> SolveReport:
     """PCG on this rank's z-slab of the canonical field (kx, ky, kz: local
     planes, x-fastest).  grid = (nx, ny, nzg, lx, ly, lz), the canonical
     global grid.  Every rank returns the same report.
@@ -539,9 +582,12 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
             return
         if not fused:
             ops.run(SLAB_PACK, 0, send)
-        comm.alltoall(recv, send)
-        ops.run(SLAB_ZSOLVE, 0, recv)
-        comm.alltoall(send, recv)
+        if comm.size == 1:  # one rank: the pencil is the slab, the all-to-alls are identities
+            ops.run(SLAB_ZSOLVE, 0, send)
+        else:
+            comm.alltoall(recv, send)
+            ops.run(SLAB_ZSOLVE, 0, recv)
+            comm.alltoall(send, recv)
         if not fused:
             ops.run(SLAB_UNPACK, 0, send)
         comm.allreduce(xbuf[4:5])
@@ -556,6 +602,11 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
     zsolve_and_back(True)
     it = 0
     done = False
+    # the host reads the device state only where convergence is predicted
+    # (check_every: a fixed period instead); in between it enqueues the next
+    # iterations' stages and collectives without waiting, and after the
+    # device has set Ctl.done the stage kernels return at once
+    nxt = 1
     while not done and it < max_iter:
         it += 1
         ops.run(SLAB_STENCIL, it)
@@ -565,9 +616,10 @@ def slab_solve(ops, comm, kx, ky, kz, grid, p_in=1.0, p_out=0.0, rtol=1e-9, ref_
         comm.allreduce(xbuf[3:4])
         ops.run(SLAB_FINALIZE, FIN_UPDATE)
         zsolve_and_back(False)
-        if it % check_every == 0 or it == max_iter:
-            info, _ = ops.status(max_iter)
+        if it >= nxt or it == max_iter:
+            info, hist = ops.status(max_iter)
             done = info.pad_ != 0
+            nxt = it + check_every if check_every else _next_check(it, hist, rtol)
     info, history = ops.status(max_iter)
     if info.status:
         raise PcgBreakdownError(_BREAKDOWN_MSG.get(info.breakdown_kind, "breakdown"), info.breakdown_iter)
@@ -630,62 +682,122 @@ def release_slab_plans() -> None:
     release_ipc()
 
 
-def _canonical(fld, axis: str):
-    """axis_permute (pipeline.py:87-111) on CUDA tensors: returns the
-    canonical (kx, ky, kz) cubes (nz', ny', nx') and the canonical grid."""
-    g = fld.grid
-    cube = lambda a: a.reshape(g.nz, g.ny, g.nx)
-    kx, ky, kz = cube(fld.kx), cube(fld.ky), cube(fld.kz)
-    perm = lambda a, order: a.transpose(order) if isinstance(a, np.ndarray) else a.permute(*order)
-    if axis == "z":
-        return (kx, ky, kz), (g.nx, g.ny, g.nz, g.lx, g.ly, g.lz)
+def _transpose_slab(local, axis: str, comm, nx: int, ny: int, nz: int):
+    """axis_permute (pipeline.py:87-111) of a z-slab-distributed cube as one
+    all-to-all: `local` is this rank's original planes [k0, k0+nzl) as an
+    (nzl, ny, nx) CUDA tensor; returns its slab of the canonical cube for
+    `axis` (x: canonical (nz', ny', nx') = (nx, ny, nz); y: (ny, nz, nx)),
+    planes [r m, (r+1) m) with m = nx / P (x) or ny / P (y).  No rank ever
+    holds more than its slab (plus the send / receive blocks)."""
+    P, nzl = comm.size, nz // comm.size
     if axis == "x":
-        sw = lambda a: perm(a, (2, 1, 0))
-        return (sw(kz), sw(ky), sw(kx)), (g.nz, g.ny, g.nx, g.lz, g.ly, g.lx)
-    sw = lambda a: perm(a, (1, 0, 2))
-    return (sw(kx), sw(kz), sw(ky)), (g.nx, g.nz, g.ny, g.lx, g.lz, g.ly)
+        m = nx // P
+        send = local.permute(2, 1, 0).contiguous()            # [x][y][z_l]: destination-major blocks
+        recv = torch_empty_like_flat(send)
+        comm.alltoall(recv, send.reshape(-1))
+        return recv.reshape(P, m, ny, nzl).permute(1, 2, 0, 3).reshape(m, ny, nz).contiguous()
+    m = ny // P
+    send = local.permute(1, 0, 2).contiguous()                # [y][z_l][x]
+    recv = torch_empty_like_flat(send)
+    comm.alltoall(recv, send.reshape(-1))
+    return recv.reshape(P, m, nzl, nx).permute(1, 0, 2, 3).reshape(m, nz, nx).contiguous()
+
+
+def torch_empty_like_flat(t):
+    return _torch().empty(t.numel(), dtype=t.dtype, device=t.device)
+
+
+def canonical_slabs(local, grid, axis: str, comm):
+    """This rank's slab of the canonical field for `axis` from its slab of the
+    ORIGINAL field (kx, ky, kz as (nzl, ny, nx) tensors; kx is ky is kz marks
+    an isotropic field, moved once).  Returns ((kx', ky', kz') flat, the
+    canonical grid)."""
+    nx, ny, nz, lx, ly, lz = grid
+    kx, ky, kz = local
+    iso = kx is ky and ky is kz
+    if axis == "z":
+        flat = [a.reshape(-1) for a in (kx, ky, kz)]
+        return (flat[0], flat[0], flat[0]) if iso else tuple(flat), grid
+    if (nx if axis == "x" else ny) % comm.size:
+        raise ValueError(f"{'nx' if axis == 'x' else 'ny'} must be divisible by the number of ranks")
+    tr = lambda a: _transpose_slab(a, axis, comm, nx, ny, nz).reshape(-1)  # noqa: E731
+    if axis == "x":
+        cgrid = (nz, ny, nx, lz, ly, lx)
+        if iso:
+            t = tr(kx)
+            return (t, t, t), cgrid
+        return (tr(kz), tr(ky), tr(kx)), cgrid
+    cgrid = (nx, nz, ny, lx, lz, ly)
+    if iso:
+        t = tr(kx)
+        return (t, t, t), cgrid
+    return (tr(kx), tr(kz), tr(ky)), cgrid
+
+
+def effective_tensor_dist_slab(local, grid, comm=None, rtol: float = 1e-9, p_in: float = 1.0, p_out: float = 0.0,
+                               ref_mode: str = "opt", max_iter: int = 1024, axes: str = "xyz", device=None,
+                               zsolve=None):
+    """Multi-GPU effective tensor from distributed input: each rank passes
+    only its z-slab of the original field (`local` = (kx, ky, kz), each an
+    (nz/P, ny, nx) CUDA tensor, the same object three times for an isotropic
+    field) and the global grid (nx, ny, nz, lx, ly, lz).  Load directions
+    x and y are permuted by an all-to-all transpose of the slabs
+    (canonical_slabs), so no rank holds the whole field.  Returns
+    (kappa[3], {axis: SolveReport}) on every rank."""
+    torch = _torch()
+    comm = comm or TorchComm()
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    reports = {}
+    for ax in axes:
+        (kx, ky, kz), cgrid = canonical_slabs(local, grid, ax, comm)
+        nx, ny, nzg = cgrid[:3]
+        k0, nzl = slab_bounds(nzg, comm.size, comm.rank)
+        key = (cgrid, comm.rank, comm.size, dev.index)
+        ops = _OPS_CACHE.get(key)
+        if ops is None:
+            ops = CudaSlabOps(nx, ny, nzg, k0, nzl, comm.size, comm.rank, cgrid[3], cgrid[4], cgrid[5], dev)
+            _OPS_CACHE[key] = ops
+        reports[ax] = slab_solve(ops, comm, kx, ky, kz, cgrid, p_in, p_out, rtol, ref_mode, max_iter,
+                                 zsolve=zsolve)
+    kappa = np.array([reports[a].kappa_eff if a in reports else np.nan for a in "xyz"])
+    return kappa, reports
 
 
 def effective_tensor_dist(field, comm=None, rtol: float = 1e-9, p_in: float = 1.0, p_out: float = 0.0,
                           ref_mode: str = "opt", max_iter: int = 1024, axes: str = "xyz", device=None,
                           zsolve=None):
-    """Multi-GPU effective_tensor: every rank passes the same field (host
-    numpy or CUDA tensors); each solves its z-slab of every load direction
-    with the others over `comm` (default: torch.distributed world).  Returns
-    (kappa[3], {axis: SolveReport}) on every rank.  zsolve: "pencil" or
-    "spike" (see slab_solve)."""
+    """Multi-GPU effective_tensor from a field every rank can see (host numpy
+    or CUDA tensors): each rank takes its z-slab of the original field (one
+    copy of 1/P of it) and hands it to effective_tensor_dist_slab."""
     torch = _torch()
     from .solver import _as_field
 
     comm = comm or TorchComm()
     fld = _as_field(field)
+    g = fld.grid
     dev = torch.device(device if device is not None else "cuda")
     if dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
+    k0, nzl = slab_bounds(g.nz, comm.size, comm.rank)
+
+    def slab(a):
+        part = a.reshape(g.nz, g.ny, g.nx)[k0:k0 + nzl]
+        if isinstance(part, np.ndarray):
+            # a z-slab of a C-ordered cube is contiguous: upload it in place
+            # (pinned host memory stays a DMA source), no host-side copy
+            import warnings
+
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", UserWarning)  # frozen (read-only) field arrays
+                part = torch.from_numpy(np.ascontiguousarray(part))
+            out = torch.empty(part.shape, dtype=part.dtype, device=dev)
+            out.copy_(part)
+            return out
+        return part.to(dev).contiguous()
+
     iso = fld.kx is fld.ky and fld.ky is fld.kz
-    reports = {}
-    for ax in axes:
-        comps, grid = _canonical(fld, ax)
-        nx, ny, nzg = grid[:3]
-        k0, nzl = slab_bounds(nzg, comm.size, comm.rank)
-
-        def slab(c):
-            part = c[k0:k0 + nzl]
-            if isinstance(part, np.ndarray):
-                part = torch.from_numpy(np.array(part, copy=True))
-            return part.to(dev, non_blocking=True).contiguous().reshape(-1)
-
-        if iso:
-            t = slab(comps[0])
-            kx = ky = kz = t
-        else:
-            kx, ky, kz = (slab(c) for c in comps)
-        key = (grid, comm.rank, comm.size, dev.index)
-        ops = _OPS_CACHE.get(key)
-        if ops is None:
-            ops = CudaSlabOps(nx, ny, nzg, k0, nzl, comm.size, comm.rank, grid[3], grid[4], grid[5], dev)
-            _OPS_CACHE[key] = ops
-        reports[ax] = slab_solve(ops, comm, kx, ky, kz, grid, p_in, p_out, rtol, ref_mode, max_iter,
-                                 zsolve=zsolve)
-    kappa = np.array([reports[a].kappa_eff if a in reports else np.nan for a in "xyz"])
-    return kappa, reports
+    local = (slab(fld.kx),) * 3 if iso else tuple(slab(a) for a in (fld.kx, fld.ky, fld.kz))
+    return effective_tensor_dist_slab(local, (g.nx, g.ny, g.nz, g.lx, g.ly, g.lz), comm, rtol, p_in, p_out,
+                                      ref_mode, max_iter, axes, dev, zsolve)

@@ -134,3 +134,54 @@ def test_slab_solve_matches_single_process(size, n, C, axis, fused, zsolve):
         big = s > 1e-2
         assert np.all(np.abs(h[big] - s[big]) <= 1e-10 * s[big])
     assert all(out == res[0][1] for _, out, _ in res)  # every rank reports the same solve
+
+
+def _transpose(rank, size, port, q, dims):
+    try:
+        _init(rank, size, port)
+        from paper_2404_02433_b200.dist import TorchComm, canonical_slabs, slab_bounds
+
+        comm = TorchComm()
+        nx, ny, nz = dims
+        rng = np.random.default_rng(7)
+        cubes = [rng.standard_normal((nz, ny, nx)) for _ in range(3)]
+        k0, nzl = slab_bounds(nz, size, rank)
+        local = tuple(torch.from_numpy(np.ascontiguousarray(c[k0:k0 + nzl])) for c in cubes)
+        grid = (nx, ny, nz, 1.0, 2.0, 3.0)
+        ok, msg = True, []
+        for axis in "xyz":
+            (kx, ky, kz), cg = canonical_slabs(local, grid, axis, comm)
+            # the reference permutation (pipeline.py:87-111) of the whole cube, this rank's planes
+            if axis == "x":
+                want = [np.swapaxes(c, 0, 2) for c in (cubes[2], cubes[1], cubes[0])]
+                wg = (nz, ny, nx, 3.0, 2.0, 1.0)
+            elif axis == "y":
+                want = [np.swapaxes(c, 0, 1) for c in (cubes[0], cubes[2], cubes[1])]
+                wg = (nx, nz, ny, 1.0, 3.0, 2.0)
+            else:
+                want, wg = cubes, grid
+            c0, cl = slab_bounds(wg[2], size, rank)
+            for got, w in zip((kx, ky, kz), want):
+                ok &= np.array_equal(got.numpy(), np.ascontiguousarray(w[c0:c0 + cl]).reshape(-1))
+            ok &= cg == wg
+            iso = canonical_slabs((local[0],) * 3, grid, axis, comm)[0]
+            ok &= iso[0] is iso[1] and iso[1] is iso[2]
+            msg.append((axis, ok))
+        q.put((rank, bool(ok), None if ok else repr(msg)))
+    except Exception:  # pragma: no cover
+        import traceback
+
+        q.put((rank, False, traceback.format_exc()))
+    finally:
+        if td.is_initialized():
+            td.destroy_process_group()
+
+
+@pytest.mark.parametrize("size,dims", [(2, (4, 6, 8)), (4, (8, 4, 12)), (2, (6, 2, 4))])
+def test_distributed_axis_permute(size, dims):
+    """canonical_slabs: the x / y axis permutation of a z-slab-distributed
+    field as one all-to-all (no rank holds the whole field) equals the
+    reference's swapaxes of the whole cube, rank by rank (anisotropic and
+    isotropic fields)."""
+    for rank, ok, err in _spawn(_transpose, size, dims):
+        assert ok, (rank, err)

@@ -1,16 +1,17 @@
-// etc_kernels.cuh — device side of the B200 ETC solver (sm_100a, float64).
+// etc_kernels.cuh — shared device definitions of the B200 ETC solver
+// (sm_100a, float64): the local geometry (Geom), the device-resident PCG
+// state (Ctl), complex helpers, the deterministic block / grid reductions
+// with last-CTA finalisation, the small radix-2/4/8 DFTs and the runtime-size
+// Stockham line FFT, and the thread-block cluster helpers.
 //
-// Kernels of one PCG iteration (reference krylov.py:70-90, Alg. 1):
-//   k_stencil  : w = z + beta*w_old fused with q = A w (tpfa.py:110-131),
-//                harmonic faces on the fly (tpfa.py:29-30), dots q.w, q.q, w.w
-//   k_fx<2>    : p += alpha w, r -= alpha q, ||r||^2, then the x-axis DCT-II of
-//                r (transforms.py:83-104, Makhoul) written over q
-//   k_fy<0>    : y-axis DCT-II in place
-//   k_thomas   : per-mode tridiagonal solve along z (preconditioner.py:215-250)
-//                as a register/shared-memory partition solve, fused with
-//                r.z computed in the spectral domain (Parseval)
-//   k_fy<1>    : y-axis DCT-III in place
-//   k_bx       : x-axis DCT-III -> z (transforms.py:108-133)
+// The kernels of one PCG iteration (reference krylov.py:70-90, Alg. 1) live
+// in etc_b200.cu / etc_zsolve.cuh:
+//   k_stencil_pht / k_stencil_cp : q = A w (tpfa.py:110-131) and q.w, q.q, w.w
+//   k_fwd_q (k_fwd_c2 on z-slab ranks with peer stores) : r -= alpha q, |r|^2,
+//                 2-D DCT-II of r (transforms.py:83-104, Makhoul)
+//   k_zsolve_tma : per-mode tridiagonal solve along z (preconditioner.py:215-250)
+//                 with r.z by Parseval
+//   k_inv_q (k_inv_c2) : 2-D DCT-III, w = z + beta w_old, p += alpha w_old
 // Scalars (alpha, beta, rho, relres, breakdown state) never leave the device:
 // the last CTA of every reducing kernel finalises them (deterministic order).
 #pragma once

@@ -39,8 +39,9 @@ def cfg_tag(args) -> str:
 def bench_config(args) -> dict:
     """The workload both arms report (identical keys and values)."""
     n = args.n
-    return {"workload": f"{n}^3 random-inclusion RVE, contrast {args.contrast:g}, directions {args.axes}, "
-                        f"rtol {args.rtol:g}, f64{cfg_tag(args)}",
+    kind = "random-inclusion RVE" if args.field == "balls" else "log-uniform random field"
+    return {"workload": f"{n}^3 {kind}, contrast {args.contrast:g}, directions {args.axes}, "
+                        f"rtol {args.rtol:g}, f64{cfg_tag(args) if args.field == 'balls' else ''}",
             "n": n, "contrast": args.contrast, "rtol": args.rtol, "directions": args.axes,
             "l2": "inputs larger than L2 (one f64 vector = %.2f GB)" % (8 * n ** 3 / 1e9)}
 
@@ -48,10 +49,11 @@ def bench_config(args) -> dict:
 def metric_for(args) -> str:
     """BASELINE.json's metric for the default workload; the same wording with
     the actual size / contrast / directions / rtol otherwise."""
-    if (args.n, args.contrast, args.axes, args.rtol) == (512, 100.0, "xyz", 1e-6):
+    if (args.n, args.contrast, args.axes, args.rtol, args.field) == (512, 100.0, "xyz", 1e-6, "balls"):
         return METRIC
     ax = "/".join(args.axes)
-    return (f"PCG time-to-solution, {args.n}^3 random-inclusion RVE (contrast {args.contrast:g}), {ax}, "
+    kind = "random-inclusion RVE" if args.field == "balls" else "log-uniform random field"
+    return (f"PCG time-to-solution, {args.n}^3 {kind} (contrast {args.contrast:g}), {ax}, "
             f"rtol {args.rtol:g}")
 KCLASS = ["stencil", "update_fwd2d", "fwd2d", "zsolve", "unused", "inv2d", "setup"]
 
@@ -233,7 +235,16 @@ def run_b200(args, rank, world, local_rank):
     if dist:
         import torch.distributed as td
     n = args.n
-    field = P.gen_random_balls(n, 40, 0.05, 0.15, args.contrast, 11, device=dev)
+    if args.field == "random":
+        # a general field (every cell its own conductivity, no phase tables):
+        # log-uniform in [1/C, C], isotropic, seeded on the device
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(11)
+        u = torch.rand(n ** 3, dtype=torch.float64, device=dev, generator=gen)
+        kk = torch.exp((2.0 * u - 1.0) * float(np.log(args.contrast)))
+        field = P.OrthotropicField(P.GridSpec(n, n, n), kk, kk, kk)
+    else:
+        field = P.gen_random_balls(n, 40, 0.05, 0.15, args.contrast, 11, device=dev)
     axes = args.axes
     if dist:
         from paper_2404_02433_b200 import dist as D
@@ -310,7 +321,7 @@ def run_b200(args, rank, world, local_rank):
     # z-slab ranks run the same fused kernels (etc_slab_fused: ny / P a power of two >= 2)
     wfuse = (os.environ.get("ETC_WFUSE", "1") != "0" and n >= 128 and n & (n - 1) == 0
              and (not dist or n // world >= 2))
-    phases = wfuse and os.environ.get("ETC_PHASES", "1") != "0"  # the bench field has two phases
+    phases = wfuse and os.environ.get("ETC_PHASES", "1") != "0" and args.field == "balls"  # two phases
     bpc = bytes_per_cell(wfuse, phases)
     if dist and args.zsolve == "spike":
         # k_zsub_ends reads the slab twice (16 B/cell); k_zsub_solve moves t r/w, d' w/r and the
@@ -394,7 +405,9 @@ def run_b200(args, rank, world, local_rank):
         "metric": metric_for(args), "value": round(ms_step / 1e3, 4), "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: random-ball RVE (preset a: 40 balls r 0.05-0.15, seed 11), voxelised on device",
+        "data": ("synthetic: random-ball RVE (preset a: 40 balls r 0.05-0.15, seed 11), voxelised on device"
+                 if args.field == "balls" else
+                 "synthetic: log-uniform random field in [1/C, C] per cell (seed 11), generated on device"),
         "config": bench_config(args),
         "details": {
             "iterations": iters, "ms_per_iter": round(ms_step / max(1, total_iters), 4),
@@ -491,6 +504,9 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--axes", default="xyz")
     ap.add_argument("--cpu-n", type=int, default=256)
+    ap.add_argument("--field", choices=["balls", "random"], default="balls",
+                    help="balls: the BASELINE random-inclusion RVE (two phases: phase-table stencil); "
+                         "random: a general log-uniform field (stored-faces stencil, 40 B/cell)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slab", action="store_true", help="z-slab path even on one rank (exercises NCCL plumbing)")

@@ -81,18 +81,19 @@ def bytes_per_cell(wfuse: bool, phases: bool = False) -> dict:
     }
 
 
-NCU_PREFIX = {"stencil": "k_stencil", "update_fwd2d": "k_fwd", "zsolve": "k_thomas",
+NCU_PREFIX = {"stencil": "k_stencil", "update_fwd2d": "k_fwd", "zsolve": "k_zsolve",
               "inv2d": "k_inv"}
 
 
 def load_traffic(n: int) -> tuple[dict, str | None]:
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
     of each kernel class from the committed `ncu --set full` capture of the
-    default workload (profiles/r01/ncu_full_512_traffic.json, written by
-    profiles/ncu_summary.py); {} for other sizes."""
-    p = ROOT / "profiles" / "r01" / "ncu_full_512_traffic.json"
-    if n != 512 or not p.exists():
+    default workload (the latest profiles/rNN/ncu_full_512_traffic.json,
+    written by profiles/ncu_summary.py); {} for other sizes."""
+    caps = sorted((ROOT / "profiles").glob("r[0-9][0-9]/ncu_full_512_traffic.json"))
+    if n != 512 or not caps:
         return {}, None
+    p = caps[-1]
     d = json.loads(p.read_text())
     out = {}
     for cls, pre in NCU_PREFIX.items():

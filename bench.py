@@ -390,6 +390,36 @@ def run_b200(args, rank, world, local_rank):
                "samples": len(t_e2e),
                "api": "paper_2404_02433_b200.effective_tensor(numpy field in pinned host memory)"}
 
+    # the general-field stencil (stored faces, k_stencil_gt, 40 B/cell): the
+    # benchmark field has two phases and runs the phase-table stencil, so a
+    # log-uniform field of the same size is solved for a few iterations here
+    # and its stencil launches are timed the same way (etc_profile)
+    general = None
+    if not dist and args.field == "balls" and not args.no_general:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(11)
+        u = torch.rand(n ** 3, dtype=torch.float64, device=dev, generator=gen)
+        kr = torch.exp((2.0 * u - 1.0) * float(np.log(args.contrast)))
+        del u
+        frand = P.OrthotropicField(P.GridSpec(n, n, n), kr, kr, kr)
+        P.homogenize(frand, P.BoundaryConfig(P.Axis.Z, 1.0, 0.0), 1e-30, max_iter=3, device=dev)  # warm-up
+        h = P.get_plan(frand.grid, dev).handle
+        lib.etc_profile_read(h, ms8, cnt8, 1)
+        lib.etc_profile(h, 1)
+        P.homogenize(frand, P.BoundaryConfig(P.Axis.Z, 1.0, 0.0), 1e-30, max_iter=20, device=dev)
+        torch.cuda.synchronize()
+        lib.etc_profile(h, 0)
+        lib.etc_profile_read(h, ms8, cnt8, 1)
+        if cnt8[0] > 0:
+            avg = ms8[0] / cnt8[0]
+            gbs = 40 * n ** 3 / (avg * 1e-3) / 1e9
+            general = {"workload": f"{n}^3 log-uniform random field in [1/C, C], contrast {args.contrast:g}, z, "
+                                   "20 PCG iterations", "kernel": "k_stencil_gt (stored faces, TMA ring)",
+                       "launches": int(cnt8[0]), "ms_avg": round(avg, 5), "bytes_per_launch": 40 * n ** 3,
+                       "gbs": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 4)}
+        del frand, kr
+        P.release_plans()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         workers = os.cpu_count() or 1
@@ -417,7 +447,7 @@ def run_b200(args, rank, world, local_rank):
                             else f"z-slab x{world} (NCCL halo + spike z-solve all-gather + all-reduce)") if dist
                            else "single",
         },
-        "roofline": roofline, "kernels": kern, "e2e": e2e, "cpu_baseline": cpu,
+        "roofline": roofline, "kernels": kern, "general_field_stencil": general, "e2e": e2e, "cpu_baseline": cpu,
         "gpu_launches": launches, "clocks": clk,
     }
     if rank == 0:
@@ -509,6 +539,7 @@ def main():
                     help="balls: the BASELINE random-inclusion RVE (two phases: phase-table stencil); "
                          "random: a general log-uniform field (stored-faces stencil, 40 B/cell)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-general", action="store_true", help="skip the general-field stencil measurement")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slab", action="store_true", help="z-slab path even on one rank (exercises NCCL plumbing)")
     ap.add_argument("--zsolve", choices=["pencil", "spike"], default=None,

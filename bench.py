@@ -41,7 +41,8 @@ def bench_config(args) -> dict:
     n = args.n
     kind = "random-inclusion RVE" if args.field == "balls" else "log-uniform random field"
     return {"workload": f"{n}^3 {kind}, contrast {args.contrast:g}, directions {args.axes}, "
-                        f"rtol {args.rtol:g}, f64{cfg_tag(args) if args.field == 'balls' else ''}",
+                        f"rtol {args.rtol:g}, {args.precision}"
+                        f"{cfg_tag(args) if args.field == 'balls' and args.precision == 'f64' else ''}",
             "n": n, "contrast": args.contrast, "rtol": args.rtol, "directions": args.axes,
             "l2": "inputs larger than L2 (one f64 vector = %.2f GB)" % (8 * n ** 3 / 1e9)}
 
@@ -49,23 +50,27 @@ def bench_config(args) -> dict:
 def metric_for(args) -> str:
     """BASELINE.json's metric for the default workload; the same wording with
     the actual size / contrast / directions / rtol otherwise."""
-    if (args.n, args.contrast, args.axes, args.rtol, args.field) == (512, 100.0, "xyz", 1e-6, "balls"):
+    if (args.n, args.contrast, args.axes, args.rtol, args.field, args.precision) == (512, 100.0, "xyz", 1e-6, "balls",
+                                                                                     "f64"):
         return METRIC
     ax = "/".join(args.axes)
     kind = "random-inclusion RVE" if args.field == "balls" else "log-uniform random field"
     return (f"PCG time-to-solution, {args.n}^3 {kind} (contrast {args.contrast:g}), {ax}, "
-            f"rtol {args.rtol:g}")
+            f"rtol {args.rtol:g}" + (", precision f32" if args.precision == "f32" else ""))
 KCLASS = ["stencil", "update_fwd2d", "fwd2d", "zsolve", "unused", "inv2d", "setup"]
 
 
-def bytes_per_cell(wfuse: bool, phases: bool = False) -> dict:
-    """Algorithmic (compulsory) HBM bytes per cell per launch, f64.
+def bytes_per_cell(wfuse: bool, phases: bool = False, esz: int = 8) -> dict:
+    """Algorithmic (compulsory) HBM bytes per cell per launch, f64 (esz 8)
+    or the fused float32 solve (esz 4).
 
     wfuse (single-GPU square planes, the default): the inverse transform
     builds the search direction w = z + beta w_old itself, so the stencil
     reads w instead of z and w_old and writes only q.  phases (the field has
     at most 16 distinct conductivity triples, as every benchmark field does):
     a one-byte phase index replaces the three face arrays."""
+    if esz == 4:  # every vector and face in float32; the phase index stays one byte
+        return {"stencil": 9 if phases else 20, "update_fwd2d": 16, "fwd2d": 8, "zsolve": 8, "inv2d": 12}
     if wfuse:
         return {
             "stencil": 17 if phases else 40,  # w, idx (or tx, ty, tz) read; q written
@@ -256,7 +261,7 @@ def run_b200(args, rank, world, local_rank):
             return D.effective_tensor_dist(fld, comm, rtol=args.rtol, axes=axes, device=dev, zsolve=args.zsolve)
     else:
         def step(fld=field):
-            return P.effective_tensor(fld, rtol=args.rtol, axes=axes, device=dev)
+            return P.effective_tensor(fld, rtol=args.rtol, axes=axes, device=dev, precision=args.precision)
 
     for _ in range(args.warmup):
         kappa, reps = step()
@@ -323,7 +328,8 @@ def run_b200(args, rank, world, local_rank):
     wfuse = (os.environ.get("ETC_WFUSE", "1") != "0" and n >= 128 and n & (n - 1) == 0
              and (not dist or n // world >= 2))
     phases = wfuse and os.environ.get("ETC_PHASES", "1") != "0" and args.field == "balls"  # two phases
-    bpc = bytes_per_cell(wfuse, phases)
+    esz = 4 if args.precision == "f32" else 8
+    bpc = bytes_per_cell(wfuse, phases, esz)
     if dist and args.zsolve == "spike":
         # k_zsub_ends reads the slab twice (16 B/cell); k_zsub_solve moves t r/w, d' w/r and the
         # pivot table r (48 B/cell): 32 B/cell per launch on average
@@ -338,12 +344,12 @@ def run_b200(args, rank, world, local_rank):
         if name in bpc:
             b = bpc[name] * N
             if wfuse and name == "inv2d":  # first launch of each solve writes w = z (16 B/cell)
-                b = (16 * N * len(axes) + 24 * N * (kcnt[i] - len(axes))) / kcnt[i]
+                b = (2 * esz * N * len(axes) + 3 * esz * N * (kcnt[i] - len(axes))) / kcnt[i]
             gbs = b / (avg * 1e-3) / 1e9
             d.update(bytes_per_launch=int(b), gbs=round(gbs, 1), frac=round(gbs / peaks["hbm_gbs"], 4))
         kern[name] = d
     dom = max((k for k in kern if k in bpc), key=lambda k: kern[k]["ms_total"])
-    traffic, tsrc = load_traffic(n)
+    traffic, tsrc = load_traffic(n) if args.precision == "f64" else ({}, None)
     if not dist:
         for k, v in traffic.items():
             if k in kern:
@@ -395,7 +401,7 @@ def run_b200(args, rank, world, local_rank):
     # log-uniform field of the same size is solved for a few iterations here
     # and its stencil launches are timed the same way (etc_profile)
     general = None
-    if not dist and args.field == "balls" and not args.no_general:
+    if not dist and args.field == "balls" and not args.no_general and args.precision == "f64":
         gen = torch.Generator(device=dev)
         gen.manual_seed(11)
         u = torch.rand(n ** 3, dtype=torch.float64, device=dev, generator=gen)
@@ -435,7 +441,7 @@ def run_b200(args, rank, world, local_rank):
     line = {
         "metric": metric_for(args), "value": round(ms_step / 1e3, 4), "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64",
+        "vs_baseline": None, "dtype": args.precision,
         "data": ("synthetic: random-ball RVE (preset a: 40 balls r 0.05-0.15, seed 11), voxelised on device"
                  if args.field == "balls" else
                  "synthetic: log-uniform random field in [1/C, C] per cell (seed 11), generated on device"),
@@ -538,6 +544,8 @@ def main():
     ap.add_argument("--field", choices=["balls", "random"], default="balls",
                     help="balls: the BASELINE random-inclusion RVE (two phases: phase-table stencil); "
                          "random: a general log-uniform field (stored-faces stencil, 40 B/cell)")
+    ap.add_argument("--precision", choices=["f64", "f32"], default="f64",
+                    help="f32: the reference's single-precision study (homogenize(..., precision='f32'))")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-general", action="store_true", help="skip the general-field stencil measurement")
     ap.add_argument("--no-cpu", action="store_true")
@@ -554,6 +562,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus != world:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}: launch one process per GPU")
+    if args.precision == "f32" and (world > 1 or args.slab):
+        raise SystemExit("--precision f32 runs on single-GPU plans")
     if args.zsolve is None:
         args.zsolve = "spike" if world > 1 else "pencil"
     rank = int(os.environ.get("RANK", "0"))

@@ -30,52 +30,6 @@ __device__ __forceinline__ float harm32(float a, float b) {
   return __fdiv_rn(__fmul_rn(__fmul_rn(2.0f, a), b), __fadd_rn(a, b));
 }
 
-__device__ __forceinline__ double f32r(double v) { return (double)(float)v; }  // np.float32 result of a dot
-__device__ __forceinline__ double f32norm(double rr) { return (double)sqrtf((float)rr); }
-
-__device__ __forceinline__ void fin_stencil32(Ctl* ctl, double qw, double qq, double ww) {
-  const double eps = 1.1920928955078125e-07;  // finfo(float32).eps
-  qw = f32r(qw);
-  ctl->last_qw = qw;
-  if (qw <= 100.0 * eps * f32norm(qq) * f32norm(ww)) {  // krylov.py:72-75
-    ctl->status = 1;
-    ctl->bd_kind = BD_OPERATOR;
-    ctl->bd_iter = ctl->it + 1;
-    ctl->done = 1;
-  }
-  ctl->alpha = ctl->rho / qw;
-}
-
-__device__ __forceinline__ void fin_normb32(Ctl* ctl, double rr, double* hist) {
-  ctl->last_rr = rr;
-  ctl->norm_b = f32norm(rr);
-  if (ctl->norm_b == 0.0) {
-    hist[0] = 0.0;
-    ctl->converged = 1;
-    ctl->done = 1;
-  } else {
-    hist[0] = 1.0;
-  }
-}
-
-__device__ __forceinline__ void fin_update32(Ctl* ctl, double rr, double* hist) {
-  ctl->last_rr = rr;
-  const double rel = f32norm(rr) / ctl->norm_b;
-  if (!isfinite(rel)) {
-    ctl->status = 1;
-    ctl->bd_kind = BD_NONFINITE;
-    ctl->bd_iter = ctl->it + 1;
-    ctl->done = 1;
-    return;
-  }
-  ctl->it += 1;
-  hist[ctl->it] = rel;
-  if (rel <= ctl->rtol) {
-    ctl->converged = 1;
-    ctl->done = 1;
-  }
-}
-
 // canonical cell c = (k*ny + j)*nx + i
 struct Cell3 {
   int i, j, k;
@@ -499,6 +453,44 @@ __global__ void k32_tabs(int n, const double2* __restrict__ src, float2* __restr
     dst[i] = make_float2((float)src[i].x, (float)src[i].y);
 }
 
+// ---- float32 phase tables (the fused float32 solve's stencil).  The phase
+// index is the float64 one (k_phase_index); its float32 scaled coefficient
+// s = float32(k) / float32(h)^2 is written per phase by every cell of the
+// phase, then every cell is checked against it, so a table is used only if it
+// reproduces each float32 face of k32_faces bit for bit.
+__global__ void k32_phase_s(long long n, const double* __restrict__ kap, float h2f,
+                            const unsigned char* __restrict__ idx, float* __restrict__ stab) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x)
+    stab[idx[c]] = __fdiv_rn((float)kap[c], h2f);
+}
+__global__ void k32_phase_check(long long n, const double* __restrict__ kap, float h2f,
+                                const unsigned char* __restrict__ idx, const float* __restrict__ stab,
+                                int* __restrict__ bad) {
+  bool b = false;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x)
+    b |= stab[idx[c]] != __fdiv_rn((float)kap[c], h2f);
+  if (b) atomicExch(bad, 1);
+}
+// faces [ax][a * PH_MAX + b] = harm32(s_a, s_b) (lower cell a, as k32_faces),
+// tb[p] = 2 s_z
+__global__ void k32_phase_ftab(const float* __restrict__ stab, int m, float* __restrict__ ftab) {
+  for (int e = threadIdx.x; e < PH_MAX * PH_MAX; e += blockDim.x) {
+    const int a = e / PH_MAX, b = e % PH_MAX;
+    const bool ok = a < m && b < m;
+    for (int ax = 0; ax < 3; ++ax)
+      ftab[ax * PH_MAX * PH_MAX + e] = ok ? harm32(stab[ax * PH_MAX + a], stab[ax * PH_MAX + b]) : 0.0f;
+  }
+  for (int q = threadIdx.x; q < PH_MAX; q += blockDim.x)
+    ftab[3 * PH_MAX * PH_MAX + q] = q < m ? __fmul_rn(2.0f, stab[2 * PH_MAX + q]) : 0.0f;
+}
+
+// p += float32(alpha) w after the last iteration (krylov.py:76)
+__global__ void k32_pupdate(long long n, float* __restrict__ p, const float* __restrict__ w, const Ctl* ctl) {
+  const float af = (float)ctl->alpha;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x)
+    p[c] = __fadd_rn(p[c], __fmul_rn(af, w[c]));
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -530,6 +522,14 @@ static int f32_faces(etc_plan* pl) {
   if (pl->axis == 1) { comp[0] = 0; comp[1] = 2; comp[2] = 1; }
   const double h[3] = {pl->lx / pl->nx, pl->ly / pl->ny, pl->lz / pl->nz};
   const Geom g = geom(pl);
+  const bool ph = pl->nph > 0 && pl->fast32;
+  pl->ph32_ok = false;
+  if (ph && !pl->ftab32) {
+    if ((rc = f32_alloc(pl, &pl->ftab32, 3 * PH_MAX * PH_MAX + PH_MAX))) return rc;
+    if ((rc = f32_alloc(pl, &pl->stab32, 4 * PH_MAX))) return rc;
+  }
+  int* bad = reinterpret_cast<int*>(pl->stab32 + 3 * PH_MAX);
+  if (ph) CK(cudaMemsetAsync(bad, 0, sizeof(int), pl->stream));
   for (int a = 0; a < 3; ++a) {
     // the permuted conductivity (scale 1) into the f64 scratch z, then faces
     if ((rc = scale_into(pl, pl->raw[comp[a]], 1.0, pl->z))) return rc;
@@ -538,6 +538,20 @@ static int f32_faces(etc_plan* pl) {
     Tm tm(pl, 6);
     k32_faces<<<grid1d(pl, pl->n), 256, 0, pl->stream>>>(g, a, pl->z, h2f, pl->v32[a], pl->tb32);
     CK(cudaGetLastError());
+    if (ph) {
+      k32_phase_s<<<grid1d(pl, pl->n), 256, 0, pl->stream>>>(pl->n, pl->z, h2f, pl->pidx, pl->stab32 + a * PH_MAX);
+      k32_phase_check<<<grid1d(pl, pl->n), 256, 0, pl->stream>>>(pl->n, pl->z, h2f, pl->pidx,
+                                                                  pl->stab32 + a * PH_MAX, bad);
+      CK(cudaGetLastError());
+    }
+  }
+  if (ph) {
+    k32_phase_ftab<<<1, 256, 0, pl->stream>>>(pl->stab32, pl->nph, pl->ftab32);
+    CK(cudaGetLastError());
+    int hb = 1;
+    CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    pl->ph32_ok = hb == 0;
   }
   pl->faces32_ok = true;
   return ETC_OK;
@@ -631,12 +645,248 @@ static int f32_set_reference(etc_plan* pl) {
   return ETC_OK;
 }
 
+// ---------------------------------------------------------------------------
+// the fused float32 solve: the float64 solve's kernels instantiated on float
+// (square power-of-two planes, N >= 128, nz = 32 L with L in {4, 8, 16}):
+//   k_stencil_pht<N, true, float> (float32 phase tables; k32_stencil with
+//     stored float32 faces when the field has more phases): q = A w, dots;
+//   k_fwd_q<N, 2, float>: r -= float32(alpha) q, |r|^2, 2-D DCT-II of r;
+//   k_zsolve_tma<L, float>: the z elimination on the float32 spectrum with
+//     the reference's float32 coefficients, pivots and sweeps in float64
+//     registers, r.z by Parseval;
+//   k_inv_q<N, true, 2, float>: 2-D DCT-III, w = z + float32(beta) w_old and
+//     p += float32(alpha) w_old on the outflow plane.
+// The transforms compute in float32 (complex64, as the reference's
+// precision study), with the float32 twiddle tables of the line passes.
+// ---------------------------------------------------------------------------
+static bool fast32_ok(etc_plan* pl) {
+  if (!pl->fast32 || pl->precond != ETC_PRECOND_FCT || pl->slab || pl->generic_fft || !pl->qplanes || !pl->ztma)
+    return false;
+  const Geom g = geom(pl);
+  const int N = ct_size(g);
+  if (N < 128 || !c2_ok(pl, ct_cfg(pl, g), N)) return false;
+  const int Lz = pl->Lz;
+  return pl->Qz == 32 && Lz * 32 == g.nz && (Lz == 4 || Lz == 8 || Lz == 16) && g.plane % 2 == 0;
+}
+
+static PlaneTabsT<float> tabs32(const etc_plan* pl) {
+  const int M = pl->maxd;
+  PlaneTabsT<float> T;
+  T.twx = pl->ctab32;
+  T.twy = pl->ctab32 + M;
+  T.ex = pl->ctab32 + 2 * M;
+  T.ey = pl->ctab32 + 3 * M;
+  return T;
+}
+
+template <int MODE>
+static int f32_fwd(const Launch& L, const float* src, float* dst, float* r, const float* q, unsigned* counter) {
+  etc_plan* pl = L.pl;
+  Tm tm(pl, MODE == 2 ? 1 : (MODE == 1 ? 6 : 2));
+  const PlaneTabsT<float> T = tabs32(pl);
+#define ETC_F32_FWD(NN)                                                                                      \
+  case NN:                                                                                                   \
+    return launch_q<NN, float>(L, k_fwd_q<NN, MODE, float>, L.g, src, dst, r, q, pl->ctl, pl->partials,      \
+                               counter, T, pl->hist, (float*)nullptr, 0);
+  switch (ct_size(L.g)) {
+    ETC_F32_FWD(128)
+    ETC_F32_FWD(256)
+    ETC_F32_FWD(512)
+    ETC_F32_FWD(1024)
+  }
+#undef ETC_F32_FWD
+  return fail(ETC_CONFIG, "fused f32 transform: unsupported plane");
+}
+
+template <int WM>
+static int f32_inv_w(const Launch& L, const float* src, float* scratch, float* w, float* p) {
+  etc_plan* pl = L.pl;
+  Tm tm(pl, 5);
+  const PlaneTabsT<float> T = tabs32(pl);
+  const int p_plane = pl->full_solution ? -1 : L.g.nz - 1;
+#define ETC_F32_INV(NN)                                                                                         \
+  case NN:                                                                                                      \
+    return launch_q<NN, float>(L, k_inv_q<NN, true, WM, float>, L.g, src, scratch, (const Ctl*)pl->ctl, T, w, p, \
+                               p_plane, (const float*)nullptr, 0);
+  switch (ct_size(L.g)) {
+    ETC_F32_INV(128)
+    ETC_F32_INV(256)
+    ETC_F32_INV(512)
+    ETC_F32_INV(1024)
+  }
+#undef ETC_F32_INV
+  return fail(ETC_CONFIG, "fused f32 inverse: unsupported plane");
+}
+
+template <int LZ>
+static int f32_zsolve_n(const Launch& L, float* t, unsigned* counter) {
+  etc_plan* pl = L.pl;
+  const Geom& g = L.g;
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(ETC_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)g.plane, (cuuint64_t)g.nz};
+  cuuint64_t strides[1] = {(cuuint64_t)g.plane * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)ZT_C, (cuuint32_t)std::min(g.nz, 256)}, es[2] = {1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, t, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return fail(ETC_CUDA, "z-solve tensor map");
+  auto kern = k_zsolve_tma<LZ, float>;
+  const size_t smem = zt_smem_bytes<LZ, float>();
+  int rc;
+  if ((rc = prep_smem(kern, smem))) return rc;
+  const long long tiles = (g.plane + ZT_C - 1) / ZT_C;
+  const int grid = (int)std::max(1LL, std::min(tiles, (long long)pl->sms));
+  // the reference's float32 z_diag and off-diagonal (preconditioner.py:178-199)
+  auto f = [](double v) { return (double)(float)v; };
+  Tm tm(pl, 3);
+  kern<<<grid, 544, smem, pl->stream>>>(g, map, L.wx, L.wy, f(pl->zd3[0]), f(pl->zd3[1]), f(pl->zd3[2]), pl->refs[0],
+                                        pl->refs[1], f(-pl->refs[2]), pl->ctl, pl->partials, counter, 1);
+  CK(cudaGetLastError());
+  return ETC_OK;
+}
+
+static int f32_zsolve(const Launch& L, float* t, unsigned* counter) {
+  switch (L.pl->Lz) {
+    case 4: return f32_zsolve_n<4>(L, t, counter);
+    case 8: return f32_zsolve_n<8>(L, t, counter);
+    case 16: return f32_zsolve_n<16>(L, t, counter);
+  }
+  return fail(ETC_CONFIG, "fused f32 z-solve: unsupported z chunk");
+}
+
+// q = A w: the float32 phase tables through the TMA-staged stencil, or the
+// stored float32 faces (k32_stencil with w as its direction)
+static int f32_stencil_w(const Launch& L, const float* w, float* q, unsigned* counter) {
+  etc_plan* pl = L.pl;
+  const Geom& g = L.g;
+  Tm tm(pl, 0);
+  if (pl->nph > 0 && pl->ph32_ok) {
+    CUtensorMap mw, mi;
+    if (plane_map(&mw, w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.nx, g.nz, PhaseStageTmaT<float>::WX, 18) &&
+        plane_map(&mi, pl->pidx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.nx, g.nz, 64, 18)) {
+      const int bx = g.nx / 32, by = g.ny / 16;
+      int ks = (int)std::max(1LL, std::min<long long>(g.nz, (2LL * 1024 + bx * by - 1) / (bx * by)));
+      const int kchunk = (g.nz + ks - 1) / ks;
+      ks = (g.nz + kchunk - 1) / kchunk;
+      dim3 grid(bx, by, ks), block(32, 8);
+      const size_t sm = ph_ft_bytes<float>() + 4 * sizeof(PhaseStageTmaT<float>) + 4 * sizeof(unsigned long long);
+#define ETC_F32_PHT(NN)                                                                                        \
+  case NN: {                                                                                                   \
+    auto kern = pl->pair32 ? k_stencil_pp<NN, true, float> : k_stencil_pht<NN, true, float>;                   \
+    int rc_;                                                                                                   \
+    if ((rc_ = prep_smem(kern, sm))) return rc_;                                                               \
+    kern<<<grid, pl->pair32 ? dim3(16, 16) : block, sm, pl->stream>>>(g, kchunk, mw, mi, pl->pidx, pl->ftab32, w, \
+                                                                      q, pl->ctl, pl->partials, counter);      \
+    CK(cudaGetLastError());                                                                                    \
+    return ETC_OK;                                                                                             \
+  }
+      switch (g.nx) {
+        ETC_F32_PHT(128)
+        ETC_F32_PHT(256)
+        ETC_F32_PHT(512)
+        ETC_F32_PHT(1024)
+      }
+#undef ETC_F32_PHT
+    }
+  }
+  const long long tiles = (long long)((pl->nx + 31) / 32) * ((pl->ny + 7) / 8);
+  const int nch = (int)std::max(1LL, std::min<long long>(pl->nz, (long long)pl->sms * 8 / std::max(1LL, tiles)));
+  const int kch = (pl->nz + nch - 1) / nch;
+  const int GS = (int)std::min<long long>(tiles * ((pl->nz + kch - 1) / kch), (long long)pl->sms * 8);
+  k32_stencil<true><<<GS, 256, 0, pl->stream>>>(g, kch, pl->v32[0], pl->v32[1], pl->v32[2], pl->tb32, w, nullptr,
+                                                 nullptr, q, pl->ctl, pl->partials, counter, 1);
+  CK(cudaGetLastError());
+  return ETC_OK;
+}
+
+// Alg. 1 on the fused float32 kernels, the float64 solve's stage order
+// (etc_solve): ||b|| and the spectrum of r, z-solve, w = z; then per
+// iteration q = A w, r / |r| / spectrum, z-solve / r.z, w and p
+static int solve32_fused(etc_plan* pl, double p_in, double p_out, double rtol, int max_iter, etc_solve_info* info,
+                         double* hist_host) {
+  Launch L = mk(pl);
+  const Geom& g = L.g;
+  float *p = pl->v32[3], *r = pl->v32[4], *q = pl->v32[5], *z = pl->v32[6], *w = pl->v32[7];
+  Ctl c;
+  std::memset(&c, 0, sizeof(c));
+  c.rtol = rtol;
+  c.max_iter = max_iter;
+  CK(cudaMemcpyAsync(pl->ctl, &c, sizeof(c), cudaMemcpyHostToDevice, pl->stream));
+  CK(cudaMemsetAsync(pl->counters, 0, 64 * sizeof(unsigned), pl->stream));
+  int rc;
+  {
+    Tm tm(pl, 6);
+    k32_rhs<<<grid1d(pl, pl->n), 256, 0, pl->stream>>>(g, pl->tb32, (float)p_in, (float)p_out, r, p, pl->ctl,
+                                                       pl->partials, pl->counters + 3, pl->hist);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(pl->ev0, pl->stream));
+  // iteration 0: ||b||, z = M r, rho = r.z, w = z (krylov.py:56-68)
+  if ((rc = f32_fwd<1>(L, r, q, nullptr, nullptr, pl->counters + 1))) return rc;
+  if ((rc = f32_zsolve(L, q, pl->counters + 2))) return rc;
+  if ((rc = f32_inv_w<1>(L, q, z, w, p))) return rc;
+  int it = 0;
+  bool done = false;
+  while (!done && it < max_iter) {
+    const int batch = std::min(pl->check_every, max_iter - it);
+    for (int b = 0; b < batch; ++b, ++it) {
+      if ((rc = f32_stencil_w(L, w, q, pl->counters + 0))) return rc;
+      if ((rc = f32_fwd<2>(L, nullptr, q, r, q, pl->counters + 1))) return rc;
+      if ((rc = f32_zsolve(L, q, pl->counters + 2))) return rc;
+      if ((rc = f32_inv_w<2>(L, q, z, w, p))) return rc;
+    }
+    CK(cudaMemcpyAsync(pl->ctl_host, pl->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pl->stream));
+    CK(cudaStreamSynchronize(pl->stream));
+    done = pl->ctl_host->done != 0;
+  }
+  CK(cudaMemcpyAsync(pl->ctl_host, pl->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pl->stream));
+  CK(cudaStreamSynchronize(pl->stream));
+  const Ctl& h = *pl->ctl_host;
+  if (h.it >= 1 && !h.status) {  // iteration it's pending p += alpha w
+    Tm tm(pl, 6);
+    const long long off = pl->full_solution ? 0 : (long long)(pl->nz - 1) * g.plane;
+    const long long cnt = pl->full_solution ? pl->n : g.plane;
+    k32_pupdate<<<grid1d(pl, cnt), 256, 0, pl->stream>>>(cnt, p + off, w + off, pl->ctl);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(pl->ev1, pl->stream));
+  float ms = 0.f;
+  CK(cudaEventSynchronize(pl->ev1));
+  cudaEventElapsedTime(&ms, pl->ev0, pl->ev1);
+  std::memset(info, 0, sizeof(*info));
+  info->iterations = h.it;
+  info->converged = h.converged;
+  info->status = h.status ? ETC_BREAKDOWN : ETC_OK;
+  info->breakdown_iter = h.bd_iter;
+  info->breakdown_kind = h.bd_kind;
+  info->norm_b = h.norm_b;
+  info->device_ms = ms;
+  if (hist_host) CK(cudaMemcpy(hist_host, pl->hist, (size_t)(h.it + 1) * sizeof(double), cudaMemcpyDeviceToHost));
+  if (h.status) return fail(ETC_BREAKDOWN, "PCG breakdown");
+  {
+    Tm tm(pl, 6);
+    const float hzf = (float)(pl->lz / pl->nz);
+    k32_flux<<<grid1d(pl, g.plane, 256, 2), 256, 0, pl->stream>>>(g, pl->tb32, p, hzf, (float)p_out, pl->scal + 20,
+                                                                  pl->partials, pl->counters + 3);
+    CK(cudaGetLastError());
+  }
+  double fs = 0.0;
+  CK(cudaMemcpyAsync(&fs, pl->scal + 20, sizeof(double), cudaMemcpyDeviceToHost, pl->stream));
+  CK(cudaStreamSynchronize(pl->stream));
+  info->flux_sum = fs;
+  info->kappa_eff = pl->lz * fs / ((double)pl->nx * pl->ny * (p_in - p_out));
+  return ETC_OK;
+}
+
 static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max_iter, etc_solve_info* info,
                    double* hist_host) {
   int rc;
   if (pl->precond == ETC_PRECOND_JACOBI) return fail(ETC_CONFIG, "precision f32 supports the fct and none preconditioners");
   if (!pl->faces32_ok && (rc = f32_faces(pl))) return rc;
   if ((rc = f32_set_reference(pl))) return rc;
+  if (fast32_ok(pl)) return solve32_fused(pl, p_in, p_out, rtol, max_iter, info, hist_host);
   const Geom g = geom(pl);
   float *tx = pl->v32[0], *ty = pl->v32[1], *tz = pl->v32[2];
   float *p = pl->v32[3], *r = pl->v32[4], *q = pl->v32[5], *z = pl->v32[6];
@@ -703,6 +953,7 @@ static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max
   CK(cudaStreamSynchronize(pl->stream));
   const Ctl& h = *pl->ctl_host;
   float ms = 0.f;
+  CK(cudaEventSynchronize(pl->ev1));
   cudaEventElapsedTime(&ms, pl->ev0, pl->ev1);
   std::memset(info, 0, sizeof(*info));
   info->iterations = h.it;

@@ -49,8 +49,24 @@ struct Ctl {
 enum { BD_NONE = 0, BD_OPERATOR = 1, BD_NONFINITE = 2, BD_PRECOND = 3 };
 
 // ---------------------------------------------------------------------------
-// complex helpers
+// complex helpers (double2 for the float64 solve, float2 for precision f32)
 // ---------------------------------------------------------------------------
+template <class T>
+struct Cx;
+template <>
+struct Cx<double> {
+  using type = double2;
+};
+template <>
+struct Cx<float> {
+  using type = float2;
+};
+template <class T>
+using C2 = typename Cx<T>::type;  // complex (or pair) of T
+
+__device__ __forceinline__ double2 mkc(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ float2 mkc(float a, float b) { return make_float2(a, b); }
+
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -58,6 +74,21 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 // a * (s*i), s = +-1
 __device__ __forceinline__ double2 cmul_si(double2 a, double s) { return make_double2(-s * a.y, s * a.x); }
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmul_si(float2 a, float s) { return make_float2(-s * a.y, s * a.x); }
+
+// correctly rounded scalar ops in the reference's association order
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 
 // position of source index i in the Makhoul even/odd reordering
 // (evens ascending then odds descending; transforms.py:41-43)
@@ -131,45 +162,39 @@ __device__ __forceinline__ void grid_sum_finalize(double (&v)[NV], double* parti
 // direct DFT for non-power-of-two lengths.  tw[m] = exp(-2 pi i m / N).
 // s = -1 forward, +1 inverse (no 1/N).  Returns the buffer holding the result.
 // ---------------------------------------------------------------------------
-template <int R>
-__device__ __forceinline__ void dft_small(double2 (&v)[R], double s);
-
-template <>
-__device__ __forceinline__ void dft_small<2>(double2 (&v)[2], double) {
-  double2 a = v[0], b = v[1];
-  v[0] = cadd(a, b);
-  v[1] = csub(a, b);
-}
-
-template <>
-__device__ __forceinline__ void dft_small<4>(double2 (&v)[4], double s) {
-  double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
-  double2 t2 = cadd(v[1], v[3]), t3 = cmul_si(csub(v[1], v[3]), s);
-  v[0] = cadd(t0, t2);
-  v[2] = csub(t0, t2);
-  v[1] = cadd(t1, t3);
-  v[3] = csub(t1, t3);
-}
-
-template <>
-__device__ __forceinline__ void dft_small<8>(double2 (&v)[8], double s) {
-  const double h = 0.70710678118654752440;
-  double2 u[4], d[4];
+template <int R, class C, class S>
+__device__ __forceinline__ void dft_small(C (&v)[R], S s) {
+  if constexpr (R == 2) {
+    C a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    C t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    C t2 = cadd(v[1], v[3]), t3 = cmul_si(csub(v[1], v[3]), s);
+    v[0] = cadd(t0, t2);
+    v[2] = csub(t0, t2);
+    v[1] = cadd(t1, t3);
+    v[3] = csub(t1, t3);
+  } else {
+    static_assert(R == 8, "radix 2, 4 or 8");
+    const S h = (S)0.70710678118654752440;
+    C u[4], d[4];
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    u[m] = cadd(v[m], v[m + 4]);
-    d[m] = csub(v[m], v[m + 4]);
-  }
-  // d[m] *= W^m, W = exp(s 2 pi i / 8)
-  d[1] = make_double2(h * (d[1].x - s * d[1].y), h * (d[1].y + s * d[1].x));
-  d[2] = cmul_si(d[2], s);
-  d[3] = make_double2(-h * (d[3].x + s * d[3].y), h * (s * d[3].x - d[3].y));
-  dft_small<4>(u, s);
-  dft_small<4>(d, s);
+    for (int m = 0; m < 4; ++m) {
+      u[m] = cadd(v[m], v[m + 4]);
+      d[m] = csub(v[m], v[m + 4]);
+    }
+    // d[m] *= W^m, W = exp(s 2 pi i / 8)
+    d[1] = mkc(h * (d[1].x - s * d[1].y), h * (d[1].y + s * d[1].x));
+    d[2] = cmul_si(d[2], s);
+    d[3] = mkc(-h * (d[3].x + s * d[3].y), h * (s * d[3].x - d[3].y));
+    dft_small<4>(u, s);
+    dft_small<4>(d, s);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    v[2 * q] = u[q];
-    v[2 * q + 1] = d[q];
+    for (int q = 0; q < 4; ++q) {
+      v[2 * q] = u[q];
+      v[2 * q + 1] = d[q];
+    }
   }
 }
 

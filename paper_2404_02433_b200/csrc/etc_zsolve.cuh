@@ -32,12 +32,14 @@ constexpr int ZT_C = 16;       // columns per tile (one 128-byte row segment)
 constexpr int ZT_STAGES = 3;   // tile buffers per CTA
 constexpr int ZT_XS = 33;      // padded stride of the per-column exchange rows
 
-template <int L>
-constexpr size_t zt_tile_bytes() { return (size_t)32 * L * ZT_C * sizeof(double); }
-template <int L>
+// T: the type of the vector and of the elimination (double; float for
+// precision f32, which eliminates in float32 as the reference does)
+template <int L, class T = double>
+constexpr size_t zt_tile_bytes() { return (size_t)32 * L * ZT_C * sizeof(T); }
+template <int L, class T = double>
 constexpr size_t zt_smem_bytes() {
-  return ZT_STAGES * zt_tile_bytes<L>() + (size_t)2 * (2 * L + 7) * ZT_C * sizeof(double) +
-         (size_t)3 * ZT_C * ZT_XS * sizeof(double) + 8 * ZT_STAGES;
+  return ZT_STAGES * zt_tile_bytes<L, T>() + (size_t)2 * (2 * L + 7) * ZT_C * sizeof(T) +
+         (size_t)3 * ZT_C * ZT_XS * sizeof(T) + 8 * ZT_STAGES;
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, unsigned long long* bar) {
@@ -65,40 +67,42 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // per-tile column tables, built by the producer warp one tile ahead: the
 // reciprocal pivots and spike end values depend on the column's shift only,
 // not on the data, so the 16 compute warps never run the pivot recurrence
-template <int L>
+template <int L, class R = double>
 struct ZtTab {
-  double rf[L - 1][ZT_C];  // first block (q = 0): reciprocal pivots of rows 0..L-2
-  double ri[L][ZT_C];      // other blocks: rows 0..L-2; [L-1] the last block's row L-1
+  R rf[L - 1][ZT_C];  // first block (q = 0): reciprocal pivots of rows 0..L-2
+  R ri[L][ZT_C];      // other blocks: rows 0..L-2; [L-1] the last block's row L-1
   // 0 v_last (first block) | 1 u_first 2 v_first 3 v_last (interior blocks) |
   // 4 u_first 5 v_first (last block) | 6 z_diag interior + shift | 7 r.z weight (0: column past the plane)
-  double sv[8][ZT_C];
+  R sv[8][ZT_C];
 };
 
 // map: 2-D tensor map over t viewed as (nz rows) x (plane columns), box
 // ZT_C x BR (BR = min(nz, 256) rows).  Warps 0-15 solve, warp 16 (the
 // producer) builds the next tile's tables and drives the TMA ring.
-template <int L>
+template <int L, class T = double>
 __global__ void __launch_bounds__(544, 1)
     k_zsolve_tma(Geom g, const __grid_constant__ CUtensorMap map, const double* __restrict__ wx,
-                 const double* __restrict__ wy, double zd0, double zdi, double zdl, double kxr, double kyr, double off,
+                 const double* __restrict__ wy, double zd0_, double zdi_, double zdl_, double kxr, double kyr, double off_,
                  Ctl* ctl, double* partials, unsigned* counter, int pcg) {
   static_assert(L >= 3, "blocks of at least three rows");
+  using R = T;  // float32 solve: the elimination in float32, as the reference's
+  const R zd0 = (R)zd0_, zdi = (R)zdi_, zdl = (R)zdl_, off = (R)off_;
   if (pcg && ctl->done) return;
   constexpr int Q = 32, NZ = Q * L, TC = ZT_C, S = ZT_STAGES;
   constexpr int BR = NZ < 256 ? NZ : 256, NB = NZ / BR;  // TMA boxes per tile
-  constexpr unsigned TILE_TX = (unsigned)zt_tile_bytes<L>();
+  constexpr unsigned TILE_TX = (unsigned)zt_tile_bytes<L, T>();
   extern __shared__ __align__(128) double zsm[];
-  double* tiles = zsm;                                    // S x [NZ][TC]
-  ZtTab<L>* tab = reinterpret_cast<ZtTab<L>*>(zsm + (size_t)S * NZ * TC);  // 2 stages
-  double* X = reinterpret_cast<double*>(tab + 2);         // [2][TC][ZT_XS]: g_first, d partial
-  double* SX = X + 2 * TC * ZT_XS;                        // [TC][ZT_XS] separator values
+  T* tiles = reinterpret_cast<T*>(zsm);                   // S x [NZ][TC]
+  ZtTab<L, R>* tab = reinterpret_cast<ZtTab<L, R>*>(tiles + (size_t)S * NZ * TC);  // 2 stages
+  R* X = reinterpret_cast<R*>(tab + 2);         // [2][TC][ZT_XS]: g_first, d partial
+  R* SX = X + 2 * TC * ZT_XS;                        // [TC][ZT_XS] separator values
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(SX + TC * ZT_XS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool producer = warp == TC;
   const long long plane = g.plane;
   const long long ntiles = (plane + TC - 1) / TC;
   const long long G = gridDim.x;
-  const double off2 = off * off;
+  const R off2 = off * off;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -118,56 +122,58 @@ __global__ void __launch_bounds__(544, 1)
   auto tables = [&](long long n) {
     const long long tl = blockIdx.x + n * G;
     if (tl >= ntiles) return;
-    ZtTab<L>& T = tab[n & 1];
+    ZtTab<L, R>& Tp = tab[n & 1];
     const int c = lane & 15, v = lane >> 4;
     const long long col = tl * TC + c;
     const bool valid = col < plane;
     const unsigned cu = valid ? (unsigned)col : 0u;
     const int ip = (int)(cu % (unsigned)g.nx), jp = (int)(cu / (unsigned)g.nx) + g.jofs;
-    const double shift = __dadd_rn(__dmul_rn(wx[ip], kxr), __dmul_rn(wy[jp], kyr));
-    const double B = zdi + shift;
-    double r[L];
+    // precision f32: the shift is formed in float64 and cast, z_diag + shift
+    // and the elimination run in float32 (preconditioner.py:184-250)
+    const R shift = (R)__dadd_rn(__dmul_rn(wx[ip], kxr), __dmul_rn(wy[jp], kyr));
+    const R B = zdi + shift;
+    R r[L];
     r[0] = rcp_fast((v == 0 ? zd0 : zdi) + shift);
 #pragma unroll
     for (int i = 1; i < L - 1; ++i) r[i] = rcp_fast(B - off2 * r[i - 1]);
     // spike end values of a block of L-1 rows (first / interior)
-    const double v_last = r[L - 2];
-    double mu = 1.0, vprod = v_last;
+    const R v_last = r[L - 2];
+    R mu = (R)1, vprod = v_last;
 #pragma unroll
     for (int i = L - 3; i >= 0; --i) {
-      const double cpi = off * r[i];
-      mu = 1.0 + cpi * off * r[i + 1] * mu;
+      const R cpi = off * r[i];
+      mu = (R)1 + cpi * off * r[i + 1] * mu;
       vprod = -cpi * vprod;
     }
     if (v == 0) {
 #pragma unroll
-      for (int i = 0; i < L - 1; ++i) T.rf[i][c] = r[i];
-      T.sv[0][c] = v_last;
+      for (int i = 0; i < L - 1; ++i) Tp.rf[i][c] = r[i];
+      Tp.sv[0][c] = v_last;
     } else {
 #pragma unroll
-      for (int i = 0; i < L - 1; ++i) T.ri[i][c] = r[i];
-      T.sv[1][c] = r[0] * mu;
-      T.sv[2][c] = vprod;
-      T.sv[3][c] = v_last;
+      for (int i = 0; i < L - 1; ++i) Tp.ri[i][c] = r[i];
+      Tp.sv[1][c] = r[0] * mu;
+      Tp.sv[2][c] = vprod;
+      Tp.sv[3][c] = v_last;
       // the last block: L rows, row L-1 on z_diag[nz-1]
-      const double rl = rcp_fast(zdl + shift - off2 * r[L - 2]);
-      T.ri[L - 1][c] = rl;
-      double mul = 1.0, vpl = rl;
+      const R rl = rcp_fast(zdl + shift - off2 * r[L - 2]);
+      Tp.ri[L - 1][c] = rl;
+      R mul = (R)1, vpl = rl;
       {
-        const double cpi = off * r[L - 2];
-        mul = 1.0 + cpi * off * rl * mul;
+        const R cpi = off * r[L - 2];
+        mul = (R)1 + cpi * off * rl * mul;
         vpl = -cpi * vpl;
       }
 #pragma unroll
       for (int i = L - 3; i >= 0; --i) {
-        const double cpi = off * r[i];
-        mul = 1.0 + cpi * off * r[i + 1] * mul;
+        const R cpi = off * r[i];
+        mul = (R)1 + cpi * off * r[i + 1] * mul;
         vpl = -cpi * vpl;
       }
-      T.sv[4][c] = r[0] * mul;
-      T.sv[5][c] = vpl;
-      T.sv[6][c] = B;
-      T.sv[7][c] = valid ? (ip == 0 ? 0.5 : 1.0) * (jp == 0 ? 0.5 : 1.0) : 0.0;
+      Tp.sv[4][c] = r[0] * mul;
+      Tp.sv[5][c] = vpl;
+      Tp.sv[6][c] = B;
+      Tp.sv[7][c] = valid ? (ip == 0 ? 0.5 : 1.0) * (jp == 0 ? 0.5 : 1.0) : 0.0;
     }
   };
   double dot = 0.0;
@@ -203,91 +209,91 @@ __global__ void __launch_bounds__(544, 1)
       const long long tl = blockIdx.x + n * G;
       if (tl >= ntiles) break;
       const int s = (int)(n % S);
-      double* tile = tiles + (size_t)s * NZ * TC;
-      const ZtTab<L>& T = tab[n & 1];
-      double* myf = tile + (size_t)q * L * TC + c;  // row i of the block at myf[i * TC]
+      T* tile = tiles + (size_t)s * NZ * TC;
+      const ZtTab<L, R>& Tt = tab[n & 1];
+      T* myf = tile + (size_t)q * L * TC + c;  // row i of the block at myf[i * TC]
       // reciprocal pivots straight from the table (rows L-1 of the last block
       // continue the interior table); values in registers
-      const double* rp = (q == 0) ? &T.rf[0][c] : &T.ri[0][c];
-      auto rcp = [&](int i) -> double { return rp[i * TC]; };
-      double my[L];
+      const R* rp = (q == 0) ? &Tt.rf[0][c] : &Tt.ri[0][c];
+      auto rcp = [&](int i) -> R { return rp[i * TC]; };
+      R my[L];
       mbar_wait(&bar[s], (unsigned)((n / S) & 1));
       // local forward elimination; rows 0..L-2 in every block, row L-1 only in the last
-      double xp = myf[0] * rcp(0);
+      R xp = (R)myf[0] * rcp(0);
       my[0] = xp;
 #pragma unroll
       for (int i = 1; i < L - 1; ++i) {
-        xp = (myf[i * TC] - off * xp) * rcp(i);
+        xp = ((R)myf[i * TC] - off * xp) * rcp(i);
         my[i] = xp;
       }
       if (last) {
-        xp = (myf[(L - 1) * TC] - off * xp) * rcp(L - 1);
+        xp = ((R)myf[(L - 1) * TC] - off * xp) * rcp(L - 1);
         my[L - 1] = xp;
       }
       // g = block^-1 f at the block's ends
-      const double g_last = xp;
-      double gacc = g_last;
+      const R g_last = xp;
+      R gacc = g_last;
       if (last) gacc = my[L - 2] - off * rcp(L - 2) * gacc;
 #pragma unroll
       for (int i = L - 3; i >= 0; --i) gacc = my[i] - off * rcp(i) * gacc;
       {
         const int xo = c * ZT_XS + q;
         X[xo] = gacc;                                                     // g_first
-        if (!last) X[TC * ZT_XS + xo] = myf[(L - 1) * TC] - off * g_last;  // separator rhs minus own coupling
+        if (!last) X[TC * ZT_XS + xo] = (R)myf[(L - 1) * TC] - off * g_last;  // separator rhs minus own coupling
       }
       asm volatile("bar.sync 1, 512;" ::: "memory");
       {  // warp `warp` solves the separator system of column `warp`, lane = block
         const int cw = warp, qq = lane;
         const int xo = cw * ZT_XS + qq;
-        const double lo_first = (qq == 0) ? 0.0 : off, up_last = (qq == Q - 1) ? 0.0 : off;
-        const double n_ul = (qq + 1 == Q - 1) ? 0.0 : off;
-        double a = 0.0, b = 1.0, cc = 0.0, d = 0.0;
+        const R lo_first = (qq == 0) ? (R)0 : off, up_last = (qq == Q - 1) ? (R)0 : off;
+        const R n_ul = (qq + 1 == Q - 1) ? (R)0 : off;
+        R a = (R)0, b = (R)1, cc = (R)0, d = (R)0;
         if (qq < Q - 1) {  // separator row qq L + L-1
-          const double v_first = qq == 0 ? 0.0 : T.sv[2][cw];
-          const double v_l = qq == 0 ? T.sv[0][cw] : T.sv[3][cw];
-          const double n_uf = (qq + 1 == Q - 1) ? T.sv[4][cw] : T.sv[1][cw];
-          const double n_vf = (qq + 1 == Q - 1) ? T.sv[5][cw] : T.sv[2][cw];
-          const double n_gf = X[xo + 1], dpart = X[TC * ZT_XS + xo];
+          const R v_first = qq == 0 ? (R)0 : Tt.sv[2][cw];
+          const R v_l = qq == 0 ? Tt.sv[0][cw] : Tt.sv[3][cw];
+          const R n_uf = (qq + 1 == Q - 1) ? Tt.sv[4][cw] : Tt.sv[1][cw];
+          const R n_vf = (qq + 1 == Q - 1) ? Tt.sv[5][cw] : Tt.sv[2][cw];
+          const R n_gf = X[xo + 1], dpart = X[TC * ZT_XS + xo];
           a = -off * lo_first * v_first;
-          b = T.sv[6][cw] - off * up_last * v_l - off2 * n_uf;
+          b = Tt.sv[6][cw] - off * up_last * v_l - off2 * n_uf;
           cc = -off * n_ul * n_vf;
           d = dpart - off * n_gf;
         }
 #pragma unroll
         for (int dd = 1; dd < Q; dd <<= 1) {
-          double am = __shfl_up_sync(0xffffffffu, a, dd), bm = __shfl_up_sync(0xffffffffu, b, dd);
-          double cm = __shfl_up_sync(0xffffffffu, cc, dd), dm = __shfl_up_sync(0xffffffffu, d, dd);
-          double ap = __shfl_down_sync(0xffffffffu, a, dd), bp = __shfl_down_sync(0xffffffffu, b, dd);
-          double cp = __shfl_down_sync(0xffffffffu, cc, dd), dp = __shfl_down_sync(0xffffffffu, d, dd);
-          if (qq < dd) { am = 0.0; bm = 1.0; cm = 0.0; dm = 0.0; }
-          if (qq + dd >= Q) { ap = 0.0; bp = 1.0; cp = 0.0; dp = 0.0; }
-          const double k1 = a * rcp_fast(bm), k2 = cc * rcp_fast(bp);
-          const double na = -am * k1, nc = -cp * k2;
-          const double nbv = b - cm * k1 - ap * k2, nd = d - dm * k1 - dp * k2;
+          R am = __shfl_up_sync(0xffffffffu, a, dd), bm = __shfl_up_sync(0xffffffffu, b, dd);
+          R cm = __shfl_up_sync(0xffffffffu, cc, dd), dm = __shfl_up_sync(0xffffffffu, d, dd);
+          R ap = __shfl_down_sync(0xffffffffu, a, dd), bp = __shfl_down_sync(0xffffffffu, b, dd);
+          R cp = __shfl_down_sync(0xffffffffu, cc, dd), dp = __shfl_down_sync(0xffffffffu, d, dd);
+          if (qq < dd) { am = (R)0; bm = (R)1; cm = (R)0; dm = (R)0; }
+          if (qq + dd >= Q) { ap = (R)0; bp = (R)1; cp = (R)0; dp = (R)0; }
+          const R k1 = a * rcp_fast(bm), k2 = cc * rcp_fast(bp);
+          const R na = -am * k1, nc = -cp * k2;
+          const R nbv = b - cm * k1 - ap * k2, nd = d - dm * k1 - dp * k2;
           a = na; b = nbv; cc = nc; d = nd;
         }
         SX[xo] = d / b;
       }
       asm volatile("bar.sync 1, 512;" ::: "memory");
-      const double Sv = SX[c * ZT_XS + q];
-      const double Sm = q ? SX[c * ZT_XS + q - 1] : 0.0;
+      const R Sv = SX[c * ZT_XS + q];
+      const R Sm = q ? SX[c * ZT_XS + q - 1] : (R)0;
       // separator coupling: forward sweep of the end corrections, then back substitution
-      const double lo_first = (q == 0) ? 0.0 : off;
-      const double eta0 = -lo_first * Sm;
-      const double etaL = last ? 0.0 : -off * Sv;
+      const R lo_first = (q == 0) ? (R)0 : off;
+      const R eta0 = -lo_first * Sm;
+      const R etaL = last ? (R)0 : -off * Sv;
       {
-        double h = eta0 * rcp(0);
+        R h = eta0 * rcp(0);
         my[0] += h;
 #pragma unroll
         for (int i = 1; i < L - 1; ++i) {
-          h = ((i == L - 2 && !last ? etaL : 0.0) - off * h) * rcp(i);
+          h = ((i == L - 2 && !last ? etaL : (R)0) - off * h) * rcp(i);
           my[i] += h;
         }
         if (last) {
-          h = (0.0 - off * h) * rcp(L - 1);
+          h = ((R)0 - off * h) * rcp(L - 1);
           my[L - 1] += h;
         }
-        double xn = last ? my[L - 1] : my[L - 2];
+        R xn = last ? my[L - 1] : my[L - 2];
         if (last) {
           xn = my[L - 2] - off * rcp(L - 2) * xn;
           my[L - 2] = xn;
@@ -304,10 +310,10 @@ __global__ void __launch_bounds__(544, 1)
         double sacc = 0.0;
 #pragma unroll
         for (int i = 0; i < L; ++i) {
-          sacc = fma(myf[i * TC], my[i], sacc);
-          myf[i * TC] = my[i];
+          sacc = fma((double)myf[i * TC], (double)my[i], sacc);
+          myf[i * TC] = (T)my[i];
         }
-        if (pcg) dot = fma(T.sv[7][c], sacc, dot);
+        if (pcg) dot = fma((double)Tt.sv[7][c], sacc, dot);
       }
       fence_proxy_async_smem();  // the generic-proxy writes are seen by the TMA store
       __syncthreads();
@@ -319,6 +325,8 @@ __global__ void __launch_bounds__(544, 1)
     grid_sum_finalize<1>(v, partials, counter, [&](double (&tt)[1]) {
       if (ctl->dist)
         ctl->xbuf[4] = tt[0];
+      else if constexpr (sizeof(T) == 4)
+        fin_thomas(ctl, f32r(tt[0] * scale));  // np.dot of two float32 vectors
       else
         fin_thomas(ctl, tt[0] * scale);
     });

@@ -398,13 +398,13 @@ def _homogenize_composed(field, boundary, rtol, kind, ref_mode, precision, omega
 
 def effective_tensor(field, rtol: float = 1e-9, p_in: float = 1.0, p_out: float = 0.0,
                      ref_mode: str = "opt", max_iter: int = 1024, device=None, axes="xyz",
-                     precond: str = "fct"):
+                     precond: str = "fct", precision: str = "f64"):
     """Diagonal effective-conductivity tensor from one solve per load
     direction (the reference composes it from three homogenize() calls,
     pkg/tests/test_pipeline.py:54-58).  The field is uploaded once."""
     reports = {}
     for ax in axes:
         reports[ax] = homogenize(field, BoundaryConfig(Axis(ax), p_in, p_out), rtol, precond,
-                                 ref_mode, "f64", 1.0, max_iter, device)
+                                 ref_mode, precision, 1.0, max_iter, device)
     kappa = np.array([reports[a].kappa_eff if a in reports else np.nan for a in "xyz"])
     return kappa, reports

@@ -791,6 +791,38 @@ static int f32_stencil_w(const Launch& L, const float* w, float* q, unsigned* co
 #undef ETC_F32_PHT
     }
   }
+  if (pl->gen_tma) {  // stored float32 faces through the TMA ring (k_stencil_gt on float)
+    constexpr int WX = GenStageTmaT<float>::WX;
+    CUtensorMap mw, mx, my, mt;
+    if (plane_map(&mw, w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.nx, g.nz, WX, 18) &&
+        plane_map(&mx, pl->v32[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.nx, g.nz, WX, 18) &&
+        plane_map(&my, pl->v32[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.nx, g.nz, WX, 18) &&
+        plane_map(&mt, pl->v32[2], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.nx, g.nz, WX, 18)) {
+      const int bx = g.nx / 32, by = g.ny / 16;
+      int ks = (int)std::max(1LL, std::min<long long>(g.nz, (2LL * 1024 + bx * by - 1) / (bx * by)));
+      const int kchunk = (g.nz + ks - 1) / ks;
+      ks = (g.nz + kchunk - 1) / kchunk;
+      dim3 grid(bx, by, ks), block(32, 8);
+      const size_t sm = 4 * sizeof(GenStageTmaT<float>) + 4 * sizeof(unsigned long long);
+#define ETC_F32_GT(NN)                                                                                        \
+  case NN: {                                                                                                  \
+    auto kern = k_stencil_gt<NN, true, float>;                                                                \
+    int rc_;                                                                                                  \
+    if ((rc_ = prep_smem(kern, sm))) return rc_;                                                              \
+    kern<<<grid, block, sm, pl->stream>>>(g, kchunk, mw, mx, my, mt, w, pl->v32[2], pl->tb32, q, pl->ctl,    \
+                                          pl->partials, counter);                                            \
+    CK(cudaGetLastError());                                                                                   \
+    return ETC_OK;                                                                                            \
+  }
+      switch (g.nx) {
+        ETC_F32_GT(128)
+        ETC_F32_GT(256)
+        ETC_F32_GT(512)
+        ETC_F32_GT(1024)
+      }
+#undef ETC_F32_GT
+    }
+  }
   const long long tiles = (long long)((pl->nx + 31) / 32) * ((pl->ny + 7) / 8);
   const int nch = (int)std::max(1LL, std::min<long long>(pl->nz, (long long)pl->sms * 8 / std::max(1LL, tiles)));
   const int kch = (pl->nz + nch - 1) / nch;

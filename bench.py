@@ -331,9 +331,10 @@ def run_b200(args, rank, world, local_rank):
     esz = 4 if args.precision == "f32" else 8
     bpc = bytes_per_cell(wfuse, phases, esz)
     if dist and args.zsolve == "spike":
-        # k_zsub_ends reads the slab twice (16 B/cell); k_zsub_solve moves t r/w, d' w/r and the
-        # pivot table r (48 B/cell): 32 B/cell per launch on average
-        bpc["zsolve"] = 32
+        # compulsory traffic only (re-reads are not algorithmic): k_zsub_ends reads the slab once
+        # (8 B/cell; it reads it twice), k_zsub_solve moves t r/w, d' w/r and the pivot table r
+        # (40 B/cell; it reads t twice): 24 B/cell per launch on average
+        bpc["zsolve"] = 24
     peaks = load_peaks()
     kern = {}
     for i, name in enumerate(KCLASS):

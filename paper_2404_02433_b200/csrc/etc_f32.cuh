@@ -460,8 +460,21 @@ __global__ void k32_tabs(int n, const double2* __restrict__ src, float2* __restr
 // reproduces each float32 face of k32_faces bit for bit.
 __global__ void k32_phase_s(long long n, const double* __restrict__ kap, float h2f,
                             const unsigned char* __restrict__ idx, float* __restrict__ stab) {
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x)
-    stab[idx[c]] = __fdiv_rn((float)kap[c], h2f);
+  // each CTA gathers its phases' values in shared memory and writes each once
+  // (every cell storing to the same PH_MAX global words serialises on them)
+  __shared__ float sv[PH_MAX];
+  __shared__ int seen[PH_MAX];
+  if (threadIdx.x < PH_MAX) seen[threadIdx.x] = 0;
+  __syncthreads();
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+    const int p = idx[c];
+    if (!seen[p]) {
+      sv[p] = __fdiv_rn((float)kap[c], h2f);
+      seen[p] = 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < PH_MAX && seen[threadIdx.x]) stab[threadIdx.x] = sv[threadIdx.x];
 }
 __global__ void k32_phase_check(long long n, const double* __restrict__ kap, float h2f,
                                 const unsigned char* __restrict__ idx, const float* __restrict__ stab,

@@ -11,12 +11,13 @@ from collections import Counter
 from pathlib import Path
 
 LIB = Path(__file__).resolve().parents[1] / "paper_2404_02433_b200" / "libetc_b200.so"
-HOT = ["k_stencil_pht<512, 1>", "k_stencil_gt<512, 1>", "k_stencil_cp<512, 1, 1>", "k_fwd_q<512, 2>",
-       "k_inv_q<512, 1, 2>", "k_zsolve_tma<16>", "k_thomas_x<16, 8>", "k_fwd_c2<512, 2>", "k_inv_c2<512, 1, 2>",
-       "k_zsub_ends",
-       "k_zsub_solve", "k_op_stencil<double", "k_op_thomas<double", "k_op_ssor"]
+HOT = ["k_stencil_pht<512, 1, ", "k_stencil_pp<512, 1, ", "k_stencil_gt<512, 1, ", "k_stencil_cp<512, 1, 1>",
+       "k_fwd_q<512, 2, ", "k_inv_q<512, 1, 2, ", "k_zsolve_tma<16, ", "k_thomas_x<16, 8>", "k_fwd_c2<512, 2>",
+       "k_inv_c2<512, 1, 2>", "k_zsub_ends", "k_zsub_solve", "k_op_stencil<double", "k_op_thomas<double",
+       "k_op_ssor"]
+OPS_F32 = ["FFMA", "FADD", "FMUL"]
 OPS = ["UTMALDG", "UTMASTG", "UBLKCP", "UTMAPF", "LDGSTS", "LDG", "STG", "LDS", "STS", "LDL", "STL", "DFMA",
-       "DADD", "DMUL", "MUFU", "SHFL", "BAR", "SYNCS", "RED", "ATOM", "UCGABAR"]
+       "DADD", "DMUL", "FFMA", "FADD", "FMUL", "MUFU", "SHFL", "BAR", "SYNCS", "RED", "ATOM", "UCGABAR"]
 
 
 def main():
@@ -32,7 +33,7 @@ def main():
         if not any(h in name for h in HOT):
             continue
         c = Counter(m.split(".")[0] for m in re.findall(r"\b([A-Z][A-Z0-9_]+(?:\.[A-Z0-9_]+)*)\b", body))
-        print(f"{name.split('(')[0].replace('void ', '')[:40]:<40} | " + " ".join(f"{op}={c[op]}" for op in OPS if c[op]))
+        print(f"{name.split('(')[0].replace('void ', '')[:44]:<44} | " + " ".join(f"{op}={c[op]}" for op in OPS if c[op]))
 
 
 if __name__ == "__main__":

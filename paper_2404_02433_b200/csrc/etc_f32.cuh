@@ -497,6 +497,41 @@ __global__ void k32_phase_ftab(const float* __restrict__ stab, int m, float* __r
     ftab[3 * PH_MAX * PH_MAX + q] = q < m ? __fmul_rn(2.0f, stab[2 * PH_MAX + q]) : 0.0f;
 }
 
+// Jacobi in float32 (JacobiPreconditioner, preconditioner.py:324-329): 1/diag(A)
+// in operator_diagonal's accumulation order (tpfa.py:134-147) and an IEEE
+// float32 1/d; z = r * (1/diag) with rho = r.z in the same pass
+__global__ void k32_jacobi_diag(Geom g, const float* __restrict__ tx, const float* __restrict__ ty,
+                                const float* __restrict__ tz, const float* __restrict__ tb, float* __restrict__ invd) {
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const long long P = g.plane;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < g.n; c += (long long)gridDim.x * blockDim.x) {
+    const long long k = c / P, rem = c - k * P;
+    const int j = (int)(rem / nx), i = (int)(rem - (long long)j * nx);
+    float d = 0.0f;
+    if (i > 0) d = __fadd_rn(d, tx[c - 1]);
+    if (i + 1 < nx) d = __fadd_rn(d, tx[c]);
+    if (j > 0) d = __fadd_rn(d, ty[c - nx]);
+    if (j + 1 < ny) d = __fadd_rn(d, ty[c]);
+    if (k > 0) d = __fadd_rn(d, tz[c - P]);
+    if (k + 1 < nz) d = __fadd_rn(d, tz[c]);
+    if (k == 0) d = __fadd_rn(d, tb[rem]);
+    if (k == nz - 1) d = __fadd_rn(d, tb[P + rem]);
+    invd[c] = __fdiv_rn(1.0f, d);
+  }
+}
+__global__ void k32_jacobi_rz(long long n, const float* __restrict__ r, const float* __restrict__ invd,
+                              float* __restrict__ z, Ctl* ctl, double* partials, unsigned* counter) {
+  if (ctl->done) return;
+  double s = 0.0;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+    const float v = __fmul_rn(r[c], invd[c]);
+    z[c] = v;
+    s = fma((double)r[c], (double)v, s);
+  }
+  double v[1] = {s};
+  grid_sum_finalize<1>(v, partials, counter, [&](double (&t)[1]) { fin_thomas(ctl, f32r(t[0])); });
+}
+
 // p += float32(alpha) w after the last iteration (krylov.py:76)
 __global__ void k32_pupdate(long long n, float* __restrict__ p, const float* __restrict__ w, const Ctl* ctl) {
   const float af = (float)ctl->alpha;
@@ -928,7 +963,6 @@ static int solve32_fused(etc_plan* pl, double p_in, double p_out, double rtol, i
 static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max_iter, etc_solve_info* info,
                    double* hist_host) {
   int rc;
-  if (pl->precond == ETC_PRECOND_JACOBI) return fail(ETC_CONFIG, "precision f32 supports the fct and none preconditioners");
   if (!pl->faces32_ok && (rc = f32_faces(pl))) return rc;
   if ((rc = f32_set_reference(pl))) return rc;
   if (fast32_ok(pl)) return solve32_fused(pl, p_in, p_out, rtol, max_iter, info, hist_host);
@@ -936,7 +970,27 @@ static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max
   float *tx = pl->v32[0], *ty = pl->v32[1], *tz = pl->v32[2];
   float *p = pl->v32[3], *r = pl->v32[4], *q = pl->v32[5], *z = pl->v32[6];
   float* w[2] = {pl->v32[7], pl->v32[8]};
-  const bool none = pl->precond == ETC_PRECOND_NONE;
+  const bool none = pl->precond == ETC_PRECOND_NONE, jac = pl->precond == ETC_PRECOND_JACOBI;
+  const int G_ = grid1d(pl, pl->n);
+  if (jac) {
+    if (!pl->invd32 && (rc = f32_alloc(pl, &pl->invd32, (size_t)pl->n))) return rc;
+    Tm tm(pl, 6);
+    k32_jacobi_diag<<<grid1d(pl, pl->n), 256, 0, pl->stream>>>(geom(pl), tx, ty, tz, pl->tb32, pl->invd32);
+    CK(cudaGetLastError());
+  }
+  // z = M r and rho = r.z (fct: the line passes and the z elimination, then r.z)
+  auto precond_rz = [&]() -> int {
+    if (jac) {
+      k32_jacobi_rz<<<G_, 256, 0, pl->stream>>>(pl->n, r, pl->invd32, z, pl->ctl, pl->partials, pl->counters + 2);
+      CK(cudaGetLastError());
+      return ETC_OK;
+    }
+    int rc_;
+    if (!none && (rc_ = f32_precond(pl, r, q, z, 1))) return rc_;
+    k32_rz<<<G_, 256, 0, pl->stream>>>(pl->n, r, none ? r : z, pl->ctl, pl->partials, pl->counters + 2);
+    CK(cudaGetLastError());
+    return ETC_OK;
+  };
   Ctl c;
   std::memset(&c, 0, sizeof(c));
   c.rtol = rtol;
@@ -958,9 +1012,7 @@ static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max
   }
   // iteration 0: z = M r, rho = r.z (krylov.py:63-68)
   const float* zv = none ? r : z;
-  if (!none && (rc = f32_precond(pl, r, q, z, 1))) return rc;
-  k32_rz<<<G, 256, 0, pl->stream>>>(pl->n, r, zv, pl->ctl, pl->partials, pl->counters + 2);
-  CK(cudaGetLastError());
+  if ((rc = precond_rz())) return rc;
   int it = 0;
   bool done = false;
   while (!done && it < max_iter) {
@@ -985,9 +1037,7 @@ static int solve32(etc_plan* pl, double p_in, double p_out, double rtol, int max
                                               pl->partials, pl->counters + 1, pl->hist);
         CK(cudaGetLastError());
       }
-      if (!none && (rc = f32_precond(pl, r, q, z, 1))) return rc;
-      k32_rz<<<G, 256, 0, pl->stream>>>(pl->n, r, zv, pl->ctl, pl->partials, pl->counters + 2);
-      CK(cudaGetLastError());
+      if ((rc = precond_rz())) return rc;
     }
     CK(cudaMemcpyAsync(pl->ctl_host, pl->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pl->stream));
     CK(cudaStreamSynchronize(pl->stream));

@@ -308,8 +308,6 @@ def _homogenize(field, boundary, rtol, precond, ref_mode, precision, omega, max_
             raise ConfigError("the full-solution mode runs the fused preconditioners (fct | jacobi | none)")
         return _homogenize_composed(field, boundary, rtol, kind, ref_mode, precision, omega, max_iter,
                                     device), None
-    if precision == "f32" and kind == "jacobi":
-        raise ConfigError("precision f32 runs with the fct and none preconditioners")
     if precision == "f32" and keep_solution:
         raise ConfigError("the full-solution mode runs in f64")
     if rtol <= 0.0:

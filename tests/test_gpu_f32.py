@@ -141,7 +141,8 @@ def test_f32_then_f64_on_one_plan():
     assert a.kappa_eff == b.kappa_eff
 
 
-def test_f32_jacobi_is_a_config_error():
-    f = P.gen_random_balls(8, 40, 0.05, 0.15, 10.0, 11)
-    with pytest.raises(P.ConfigError):
-        P.homogenize(f, P.BoundaryConfig(P.Axis("z"), 1.0, 0.0), 1e-5, precond="jacobi", precision="f32")
+def test_f32_jacobi_and_ssor_match_reference():
+    """Jacobi (float32 1/diag(A) in operator_diagonal's order, z = r / diag)
+    and SSOR (the plugin composition on float32 device arrays) against the
+    reference's f32 runs (tests/golden/solves_f32_jacobi.json)."""
+    _check_against_reference(json.loads((GOLDEN / "solves_f32_jacobi.json").read_text()))

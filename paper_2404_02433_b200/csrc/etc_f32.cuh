@@ -811,22 +811,27 @@ static int f32_stencil_w(const Launch& L, const float* w, float* q, unsigned* co
   const Geom& g = L.g;
   Tm tm(pl, 0);
   if (pl->nph > 0 && pl->ph32_ok) {
+    const bool r4 = pl->phry == 4 && !pl->pair32 && g.nx >= 256;  // 32-row tiles, four rows per thread
+    const int RH = r4 ? 32 : 16;
     CUtensorMap mw, mi;
-    if (plane_map(&mw, w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.nx, g.nz, PhaseStageTmaT<float>::WX, 18) &&
-        plane_map(&mi, pl->pidx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.nx, g.nz, 64, 18)) {
-      const int bx = g.nx / 32, by = g.ny / 16;
+    if (plane_map(&mw, w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.nx, g.nz, PhaseStageTmaT<float>::WX, RH + 2) &&
+        plane_map(&mi, pl->pidx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.nx, g.nz, 64, RH + 2)) {
+      const int bx = g.nx / 32, by = g.ny / RH;
       int ks = (int)std::max(1LL, std::min<long long>(g.nz, (2LL * 1024 + bx * by - 1) / (bx * by)));
       const int kchunk = (g.nz + ks - 1) / ks;
       ks = (g.nz + kchunk - 1) / kchunk;
       dim3 grid(bx, by, ks), block(32, 8);
-      const size_t sm = ph_ft_bytes<float>() + 4 * sizeof(PhaseStageTmaT<float>) + 4 * sizeof(unsigned long long);
+      const size_t sm = ph_ft_bytes<float>() +
+                        4 * (r4 ? sizeof(PhaseStageTma34f) : sizeof(PhaseStageTmaT<float>)) +
+                        4 * sizeof(unsigned long long);
 #define ETC_F32_PHT(NN)                                                                                        \
   case NN: {                                                                                                   \
-    auto kern = pl->pair32 ? k_stencil_pp<NN, true, float> : k_stencil_pht<NN, true, float>;                   \
+    auto kern = r4 ? k_stencil_pht<NN, true, float, 4>                                                         \
+                   : (pl->pair32 ? k_stencil_pp<NN, true, float> : k_stencil_pht<NN, true, float>);           \
     int rc_;                                                                                                   \
     if ((rc_ = prep_smem(kern, sm))) return rc_;                                                               \
-    kern<<<grid, pl->pair32 ? dim3(16, 16) : block, sm, pl->stream>>>(g, kchunk, mw, mi, pl->pidx, pl->ftab32, w, \
-                                                                      q, pl->ctl, pl->partials, counter);      \
+    kern<<<grid, (pl->pair32 && !r4) ? dim3(16, 16) : block, sm, pl->stream>>>(                              \
+        g, kchunk, mw, mi, pl->pidx, pl->ftab32, w, q, pl->ctl, pl->partials, counter);                       \
     CK(cudaGetLastError());                                                                                    \
     return ETC_OK;                                                                                             \
   }

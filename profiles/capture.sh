@@ -9,7 +9,7 @@ if [ "$1" = f32 ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file gpurun_out/launches512_f32.csv $CMD32 > gpurun_out/ncu_list32.log 2>&1
   timeout 1200 ncu --set full --import-source on --clock-control none \
-      -k regex:"k_stencil_pp|k_fwd_q|k_zsolve_tma|k_inv_q" -s 8 -c 4 \
+      -k regex:"k_stencil_pht|k_fwd_q|k_zsolve_tma|k_inv_q" -s 8 -c 4 \
       -o gpurun_out/prof512_f32 -f $CMD32 > gpurun_out/ncu_full32.log 2>&1
   exit 0
 fi

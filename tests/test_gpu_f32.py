@@ -146,3 +146,15 @@ def test_f32_jacobi_and_ssor_match_reference():
     and SSOR (the plugin composition on float32 device arrays) against the
     reference's f32 runs (tests/golden/solves_f32_jacobi.json)."""
     _check_against_reference(json.loads((GOLDEN / "solves_f32_jacobi.json").read_text()))
+
+def test_f32_fused_on_a_slab_shaped_grid():
+    """The fused float32 solve on a non-cubic grid (256 x 256 x 128, a general
+    field: stored faces, z-solve with L = 4) against the plain float32 kernels."""
+    g = P.GridSpec(256, 256, 128, 1.0, 1.0, 0.5)
+    rng = np.random.default_rng(7)
+    f = P.OrthotropicField(g, *np.exp(rng.uniform(-np.log(10), np.log(10), (3, 256 * 256 * 128))))
+    a = _solve_with({"ETC_FAST32": "1"}, f, "z", 1e-6)
+    b = _solve_with({"ETC_FAST32": "0"}, f, "z", 1e-6)
+    assert a.converged and b.converged and abs(a.iterations - b.iterations) <= 1
+    assert abs(a.kappa_eff - b.kappa_eff) <= 1e-5 * abs(b.kappa_eff)
+    assert a.relative_residuals != b.relative_residuals

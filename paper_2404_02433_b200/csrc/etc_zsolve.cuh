@@ -34,12 +34,14 @@ constexpr int ZT_XS = 33;      // padded stride of the per-column exchange rows
 
 // T: the type of the vector and of the elimination (double; float for
 // precision f32, which eliminates in float32 as the reference does)
-template <int L, class T = double>
-constexpr size_t zt_tile_bytes() { return (size_t)32 * L * ZT_C * sizeof(T); }
-template <int L, class T = double>
+// TC: columns per tile (16, one 128-byte row segment of doubles; 8 for
+// nz = 1024, whose 16-column tiles would not fit three stages in shared memory)
+template <int L, class T = double, int TC = ZT_C>
+constexpr size_t zt_tile_bytes() { return (size_t)32 * L * TC * sizeof(T); }
+template <int L, class T = double, int TC = ZT_C>
 constexpr size_t zt_smem_bytes() {
-  return ZT_STAGES * zt_tile_bytes<L, T>() + (size_t)2 * (2 * L + 7) * ZT_C * sizeof(T) +
-         (size_t)3 * ZT_C * ZT_XS * sizeof(T) + 8 * ZT_STAGES;
+  return ZT_STAGES * zt_tile_bytes<L, T, TC>() + (size_t)2 * (2 * L + 7) * TC * sizeof(T) +
+         (size_t)3 * TC * ZT_XS * sizeof(T) + 8 * ZT_STAGES;
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, unsigned long long* bar) {
@@ -67,20 +69,20 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // per-tile column tables, built by the producer warp one tile ahead: the
 // reciprocal pivots and spike end values depend on the column's shift only,
 // not on the data, so the 16 compute warps never run the pivot recurrence
-template <int L, class R = double>
+template <int L, class R = double, int TC = ZT_C>
 struct ZtTab {
-  R rf[L - 1][ZT_C];  // first block (q = 0): reciprocal pivots of rows 0..L-2
-  R ri[L][ZT_C];      // other blocks: rows 0..L-2; [L-1] the last block's row L-1
+  R rf[L - 1][TC];  // first block (q = 0): reciprocal pivots of rows 0..L-2
+  R ri[L][TC];      // other blocks: rows 0..L-2; [L-1] the last block's row L-1
   // 0 v_last (first block) | 1 u_first 2 v_first 3 v_last (interior blocks) |
   // 4 u_first 5 v_first (last block) | 6 z_diag interior + shift | 7 r.z weight (0: column past the plane)
-  R sv[8][ZT_C];
+  R sv[8][TC];
 };
 
 // map: 2-D tensor map over t viewed as (nz rows) x (plane columns), box
 // ZT_C x BR (BR = min(nz, 256) rows).  Warps 0-15 solve, warp 16 (the
 // producer) builds the next tile's tables and drives the TMA ring.
-template <int L, class T = double>
-__global__ void __launch_bounds__(544, 1)
+template <int L, class T = double, int TC = ZT_C>
+__global__ void __launch_bounds__(TC * 32 + 32, 1)
     k_zsolve_tma(Geom g, const __grid_constant__ CUtensorMap map, const double* __restrict__ wx,
                  const double* __restrict__ wy, double zd0_, double zdi_, double zdl_, double kxr, double kyr, double off_,
                  Ctl* ctl, double* partials, unsigned* counter, int pcg) {
@@ -88,12 +90,12 @@ __global__ void __launch_bounds__(544, 1)
   using R = T;  // float32 solve: the elimination in float32, as the reference's
   const R zd0 = (R)zd0_, zdi = (R)zdi_, zdl = (R)zdl_, off = (R)off_;
   if (pcg && ctl->done) return;
-  constexpr int Q = 32, NZ = Q * L, TC = ZT_C, S = ZT_STAGES;
+  constexpr int Q = 32, NZ = Q * L, S = ZT_STAGES, BPW = 32 / TC;  // BPW: blocks per compute warp
   constexpr int BR = NZ < 256 ? NZ : 256, NB = NZ / BR;  // TMA boxes per tile
-  constexpr unsigned TILE_TX = (unsigned)zt_tile_bytes<L, T>();
+  constexpr unsigned TILE_TX = (unsigned)zt_tile_bytes<L, T, TC>();
   extern __shared__ __align__(128) double zsm[];
   T* tiles = reinterpret_cast<T*>(zsm);                   // S x [NZ][TC]
-  ZtTab<L, R>* tab = reinterpret_cast<ZtTab<L, R>*>(tiles + (size_t)S * NZ * TC);  // 2 stages
+  ZtTab<L, R, TC>* tab = reinterpret_cast<ZtTab<L, R, TC>*>(tiles + (size_t)S * NZ * TC);  // 2 stages
   R* X = reinterpret_cast<R*>(tab + 2);         // [2][TC][ZT_XS]: g_first, d partial
   R* SX = X + 2 * TC * ZT_XS;                        // [TC][ZT_XS] separator values
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(SX + TC * ZT_XS);
@@ -122,8 +124,9 @@ __global__ void __launch_bounds__(544, 1)
   auto tables = [&](long long n) {
     const long long tl = blockIdx.x + n * G;
     if (tl >= ntiles) return;
-    ZtTab<L, R>& Tp = tab[n & 1];
-    const int c = lane & 15, v = lane >> 4;
+    ZtTab<L, R, TC>& Tp = tab[n & 1];
+    const int c = lane % TC, v = lane / TC;
+    if (v >= 2) return;  // TC = 8: lanes 16-31 idle
     const long long col = tl * TC + c;
     const bool valid = col < plane;
     const unsigned cu = valid ? (unsigned)col : 0u;
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(544, 1)
     }
     if (lane == 0) bulk_wait_all();
   } else {
-    const int c = lane & 15, q = 2 * warp + (lane >> 4);  // column in tile, block
+    const int c = lane % TC, q = BPW * warp + lane / TC;  // column in tile, block
     const bool last = (q == Q - 1);
     __syncthreads();
     for (long long n = 0;; ++n) {
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(544, 1)
       if (tl >= ntiles) break;
       const int s = (int)(n % S);
       T* tile = tiles + (size_t)s * NZ * TC;
-      const ZtTab<L, R>& Tt = tab[n & 1];
+      const ZtTab<L, R, TC>& Tt = tab[n & 1];
       T* myf = tile + (size_t)q * L * TC + c;  // row i of the block at myf[i * TC]
       // reciprocal pivots straight from the table (rows L-1 of the last block
       // continue the interior table); values in registers
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(544, 1)
         X[xo] = gacc;                                                     // g_first
         if (!last) X[TC * ZT_XS + xo] = (R)myf[(L - 1) * TC] - off * g_last;  // separator rhs minus own coupling
       }
-      asm volatile("bar.sync 1, 512;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(TC * 32) : "memory");
       {  // warp `warp` solves the separator system of column `warp`, lane = block
         const int cw = warp, qq = lane;
         const int xo = cw * ZT_XS + qq;
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(544, 1)
         }
         SX[xo] = d / b;
       }
-      asm volatile("bar.sync 1, 512;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(TC * 32) : "memory");
       const R Sv = SX[c * ZT_XS + q];
       const R Sm = q ? SX[c * ZT_XS + q - 1] : (R)0;
       // separator coupling: forward sweep of the end corrections, then back substitution

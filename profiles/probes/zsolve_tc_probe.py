@@ -1,5 +1,6 @@
 """z-solve tile width A/B: 16-column tiles, one CTA per SM (default) against
-8-column tiles, two CTAs per SM (ETC_ZTC8=1): etc_thomas outputs and time."""
+8-column tiles, two CTAs per SM (ETC_ZTC8=1, a switch of the measured build,
+removed after the measurement: profiles/r02/zsolve_tc8_rejected.log)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch

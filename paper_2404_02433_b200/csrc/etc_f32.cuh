@@ -811,7 +811,7 @@ static int f32_stencil_w(const Launch& L, const float* w, float* q, unsigned* co
   const Geom& g = L.g;
   Tm tm(pl, 0);
   if (pl->nph > 0 && pl->ph32_ok) {
-    const bool r4 = pl->phry == 4 && !pl->pair32 && g.nx >= 256;  // 32-row tiles, four rows per thread
+    const bool r4 = pl->phry == 4 && g.nx >= 256;  // 32-row tiles, four rows per thread
     const int RH = r4 ? 32 : 16;
     CUtensorMap mw, mi;
     if (plane_map(&mw, w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.nx, g.nz, PhaseStageTmaT<float>::WX, RH + 2) &&
@@ -827,10 +827,10 @@ static int f32_stencil_w(const Launch& L, const float* w, float* q, unsigned* co
 #define ETC_F32_PHT(NN)                                                                                        \
   case NN: {                                                                                                   \
     auto kern = r4 ? k_stencil_pht<NN, true, float, 4>                                                         \
-                   : (pl->pair32 ? k_stencil_pp<NN, true, float> : k_stencil_pht<NN, true, float>);           \
+                   : k_stencil_pht<NN, true, float>;                                                          \
     int rc_;                                                                                                   \
     if ((rc_ = prep_smem(kern, sm))) return rc_;                                                               \
-    kern<<<grid, (pl->pair32 && !r4) ? dim3(16, 16) : block, sm, pl->stream>>>(                              \
+    kern<<<grid, block, sm, pl->stream>>>(                                                                     \
         g, kchunk, mw, mi, pl->pidx, pl->ftab32, w, q, pl->ctl, pl->partials, counter);                       \
     CK(cudaGetLastError());                                                                                    \
     return ETC_OK;                                                                                             \

@@ -11,7 +11,7 @@ from collections import Counter
 from pathlib import Path
 
 LIB = Path(__file__).resolve().parents[1] / "paper_2404_02433_b200" / "libetc_b200.so"
-HOT = ["k_stencil_pht<512, 1, ", "k_stencil_pp<512, 1, ", "k_stencil_gt<512, 1, ", "k_stencil_cp<512, 1, 1>",
+HOT = ["k_stencil_pht<512, 1, ", "k_stencil_gt<512, 1, ", "k_stencil_cp<512, 1, 1>",
        "k_fwd_q<512, 2, ", "k_inv_q<512, 1, 2, ", "k_zsolve_tma<16, ", "k_thomas_x<16, 8>", "k_fwd_c2<512, 2>",
        "k_inv_c2<512, 1, 2>", "k_zsub_ends", "k_zsub_solve", "k_op_stencil<double", "k_op_thomas<double",
        "k_op_ssor"]

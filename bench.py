@@ -579,7 +579,13 @@ def main():
         if args.slab and "MASTER_ADDR" not in os.environ:
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29511", RANK="0", WORLD_SIZE="1")
         torch.cuda.set_device(local_rank)
-        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        import datetime
+
+        # a rank that fails or hangs surfaces as a NCCL timeout error (torch's
+        # watchdog, async error handling) within minutes instead of a stuck job
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "3")
+        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
+                              timeout=datetime.timedelta(seconds=int(os.environ.get("ETC_NCCL_TIMEOUT_S", "300"))))
     run_b200(args, rank, world, local_rank)
     if world > 1 or args.slab:
         import torch.distributed as td

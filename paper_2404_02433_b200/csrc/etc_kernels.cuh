@@ -5,7 +5,8 @@
 // Stockham line FFT, and the thread-block cluster helpers.
 //
 // The kernels of one PCG iteration (reference krylov.py:70-90, Alg. 1) live
-// in etc_b200.cu / etc_zsolve.cuh:
+// in etc_stencil.cuh, etc_planes.cuh and etc_zsolve.cuh (included by
+// etc_b200.cu; float instances for precision f32 in etc_f32.cuh):
 //   k_stencil_pht / k_stencil_cp : q = A w (tpfa.py:110-131) and q.w, q.q, w.w
 //   k_fwd_q (k_fwd_c2 on z-slab ranks with peer stores) : r -= alpha q, |r|^2,
 //                 2-D DCT-II of r (transforms.py:83-104, Makhoul)

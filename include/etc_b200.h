@@ -123,7 +123,7 @@ int etc_set_precond(etc_plan* plan, int kind);
  * operator, transforms, z elimination and PCG vectors are float32, as the
  * reference does with dtype float32; the statistics then come from the
  * float32 faces.  Single-GPU plans; fct, jacobi and none preconditioners
- * (fct on square power-of-two planes with nz = 32 L, L in {4, 8, 16}, runs
+ * (fct on square power-of-two planes with nz = 32 L, L in {4, 8, 16, 32}, runs
  * the float64 solve's fused kernels instantiated on float). */
 int etc_set_precision(etc_plan* plan, int bits);
 

@@ -714,7 +714,8 @@ static bool fast32_ok(etc_plan* pl) {
   const int N = ct_size(g);
   if (N < 128 || !c2_ok(pl, ct_cfg(pl, g), N)) return false;
   const int Lz = pl->Lz;
-  return pl->Qz == 32 && Lz * 32 == g.nz && (Lz == 4 || Lz == 8 || Lz == 16) && g.plane % 2 == 0;
+  return pl->Qz == 32 && Lz * 32 == g.nz && (Lz == 4 || Lz == 8 || Lz == 16 || (Lz == 32 && pl->z1024tma)) &&
+         g.plane % 2 == 0;
 }
 
 static PlaneTabsT<float> tabs32(const etc_plan* pl) {
@@ -766,7 +767,7 @@ static int f32_inv_w(const Launch& L, const float* src, float* scratch, float* w
   return fail(ETC_CONFIG, "fused f32 inverse: unsupported plane");
 }
 
-template <int LZ>
+template <int LZ, int TC = ZT_C>
 static int f32_zsolve_n(const Launch& L, float* t, unsigned* counter) {
   etc_plan* pl = L.pl;
   const Geom& g = L.g;
@@ -775,21 +776,21 @@ static int f32_zsolve_n(const Launch& L, float* t, unsigned* counter) {
   CUtensorMap map;
   cuuint64_t dims[2] = {(cuuint64_t)g.plane, (cuuint64_t)g.nz};
   cuuint64_t strides[1] = {(cuuint64_t)g.plane * sizeof(float)};
-  cuuint32_t box[2] = {(cuuint32_t)ZT_C, (cuuint32_t)std::min(g.nz, 256)}, es[2] = {1, 1};
+  cuuint32_t box[2] = {(cuuint32_t)TC, (cuuint32_t)std::min(g.nz, 256)}, es[2] = {1, 1};
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, t, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
       CUDA_SUCCESS)
     return fail(ETC_CUDA, "z-solve tensor map");
-  auto kern = k_zsolve_tma<LZ, float>;
-  const size_t smem = zt_smem_bytes<LZ, float>();
+  auto kern = k_zsolve_tma<LZ, float, TC>;
+  const size_t smem = zt_smem_bytes<LZ, float, TC>();
   int rc;
   if ((rc = prep_smem(kern, smem))) return rc;
-  const long long tiles = (g.plane + ZT_C - 1) / ZT_C;
+  const long long tiles = (g.plane + TC - 1) / TC;
   const int grid = (int)std::max(1LL, std::min(tiles, (long long)pl->sms));
   // the reference's float32 z_diag and off-diagonal (preconditioner.py:178-199)
   auto f = [](double v) { return (double)(float)v; };
   Tm tm(pl, 3);
-  kern<<<grid, 544, smem, pl->stream>>>(g, map, L.wx, L.wy, f(pl->zd3[0]), f(pl->zd3[1]), f(pl->zd3[2]), pl->refs[0],
+  kern<<<grid, TC * 32 + 32, smem, pl->stream>>>(g, map, L.wx, L.wy, f(pl->zd3[0]), f(pl->zd3[1]), f(pl->zd3[2]), pl->refs[0],
                                         pl->refs[1], f(-pl->refs[2]), pl->ctl, pl->partials, counter, 1);
   CK(cudaGetLastError());
   return ETC_OK;
@@ -800,6 +801,7 @@ static int f32_zsolve(const Launch& L, float* t, unsigned* counter) {
     case 4: return f32_zsolve_n<4>(L, t, counter);
     case 8: return f32_zsolve_n<8>(L, t, counter);
     case 16: return f32_zsolve_n<16>(L, t, counter);
+    case 32: return f32_zsolve_n<32, 8>(L, t, counter);  // nz = 1024: 8-column tiles
   }
   return fail(ETC_CONFIG, "fused f32 z-solve: unsupported z chunk");
 }

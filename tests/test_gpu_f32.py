@@ -158,3 +158,22 @@ def test_f32_fused_on_a_slab_shaped_grid():
     assert a.converged and b.converged and abs(a.iterations - b.iterations) <= 1
     assert abs(a.kappa_eff - b.kappa_eff) <= 1e-5 * abs(b.kappa_eff)
     assert a.relative_residuals != b.relative_residuals
+
+
+def test_f32_fused_at_1024():
+    """nz = 1024 (8-column z-solve tiles) in the fused float32 solve, against
+    the plain float32 kernels and the float64 solve of the same 1024^3 field."""
+    free, total = torch.cuda.mem_get_info()
+    if total < 150e9:  # pragma: no cover - the B200 has 180 GB
+        pytest.skip("needs a 180 GB device")
+    f = P.gen_random_balls(1024, 40, 0.05, 0.15, 100.0, 11)
+    a = _solve_with({"ETC_FAST32": "1"}, f, "z", 1e-6)
+    b = _solve_with({"ETC_FAST32": "0"}, f, "z", 1e-6)
+    c = _solve_with({}, f, "z", 1e-6, precision="f64")
+    assert a.converged and b.converged and abs(a.iterations - b.iterations) <= 1
+    assert abs(a.iterations - c.iterations) <= 2
+    assert abs(a.kappa_eff - b.kappa_eff) <= 1e-5 * abs(b.kappa_eff)
+    assert abs(a.kappa_eff - c.kappa_eff) <= 1e-4 * abs(c.kappa_eff)
+    assert a.relative_residuals != b.relative_residuals
+    del f
+    torch.cuda.empty_cache()

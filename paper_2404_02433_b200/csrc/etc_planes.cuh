@@ -664,9 +664,14 @@ template <int N>
 constexpr int c2_nt() { return N >= 1024 ? 512 : 256; }
 template <int N>
 constexpr int c2_lpc() { return c2_nt<N>() * 16 / N; }
+// line pitch (complex elements): one pad per 8 (padi) plus an offset that
+// spreads the lines a quarter-warp touches in the column phase over the
+// banks; 8-byte elements (float2) are served per half-warp and need an
+// offset of 2 there (a bank model of the passes: excess wavefronts of the
+// column phase 2.0 -> 1.03 per access at N = 512)
 template <int N, class T = double>
 constexpr int c2_pitch() {
-  return N + N / 8 + (c2_lpc<N>() >= 8 ? 1 : 8 / c2_lpc<N>());
+  return N + N / 8 + ((sizeof(T) == 4 && N >= 512) ? 2 : (c2_lpc<N>() >= 8 ? 1 : 8 / c2_lpc<N>()));
 }
 
 template <int N, bool G>

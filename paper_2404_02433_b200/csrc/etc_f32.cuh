@@ -828,7 +828,7 @@ static int f32_stencil_w(const Launch& L, const float* w, float* q, unsigned* co
                         4 * sizeof(unsigned long long);
 #define ETC_F32_PHT(NN)                                                                                        \
   case NN: {                                                                                                   \
-    auto kern = r4 ? k_stencil_pht<NN, true, float, 4>                                                         \
+    auto kern = r4 ? (pl->phcons ? k_stencil_pht<NN, true, float, 4, true> : k_stencil_pht<NN, true, float, 4>) \
                    : k_stencil_pht<NN, true, float>;                                                          \
     int rc_;                                                                                                   \
     if ((rc_ = prep_smem(kern, sm))) return rc_;                                                               \

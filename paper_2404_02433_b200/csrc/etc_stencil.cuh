@@ -532,7 +532,11 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <int N, bool PCG = true, class T = double, int RY = 2>
+// CONS: a thread's RY rows are consecutive (rows ly*RY .. ly*RY+RY-1 of the
+// tile instead of ly, ly+8, ...), so a row's y neighbours inside the group
+// are the neighbouring rows' own values and phases, already in registers,
+// and the y face between two of them is looked up once
+template <int N, bool PCG = true, class T = double, int RY = 2, bool CONS = false>
 __global__ void __launch_bounds__(256, 4)
     k_stencil_pht(Geom g, int kchunk, const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mi,
                   const unsigned char* __restrict__ pidx, const T* __restrict__ ftab, const T* __restrict__ wv,
@@ -579,7 +583,7 @@ __global__ void __launch_bounds__(256, 4)
       um[r] = 0;
       fzm[r] = 0;
       if (kg0 + k0 > 0) {  // plane k0-1 may be the lower halo
-        const long long o = (long long)(k0 - 1) * P + (long long)(j0 + ly + 8 * r) * N + i;
+        const long long o = (long long)(k0 - 1) * P + (long long)(j0 + (CONS ? ly * RY + r : ly + 8 * r)) * N + i;
         um[r] = wv[o];
         fzm[r] = FT[2 * T2 + pidx[o] * PH_RS + pidx[o + P]];
       }
@@ -587,7 +591,8 @@ __global__ void __launch_bounds__(256, 4)
     issue(k0);
     issue(k0 + 1);
     issue(k0 + 2);
-    const int wo = (j0 + ly - oy) * WX + (i - ox), io = (j0 + ly - oy) * 64 + (i - oxi);  // cell offsets, r = 0
+    const int ly0 = CONS ? ly * RY : ly, rs = CONS ? 1 : 8;  // the thread's first row, row step
+    const int wo = (j0 + ly0 - oy) * WX + (i - ox), io = (j0 + ly0 - oy) * 64 + (i - oxi);  // cell offsets, r = 0
     T ucur[RY];
     int pcur[RY];
     for (int k = k0; k < k1; ++k) {
@@ -602,14 +607,74 @@ __global__ void __launch_bounds__(256, 4)
       if (k == k0) {
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
-          ucur[r] = (&c.W[0][0])[wo + 8 * WX * r];
-          pcur[r] = (&c.I[0][0])[io + 8 * 64 * r];
+          ucur[r] = (&c.W[0][0])[wo + rs * WX * r];
+          pcur[r] = (&c.I[0][0])[io + rs * 64 * r];
         }
+      }
+      if constexpr (CONS) {
+        constexpr int R = PH_RS;
+        T unext[RY];
+        int pnext[RY];
+        T fyprev = 0;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          const int j = j0 + ly0 + r;
+          const T* Wc = &c.W[0][0] + wo + WX * r;
+          const unsigned char* Ic = &c.I[0][0] + io + 64 * r;
+          const T uc = ucur[r];
+          const int pc = pcur[r];
+          const T* FX = FT + pc;       // [a][pc]
+          const T* FXr = FT + pc * R;  // [pc][b]
+          const T fxm = FX[Ic[-1] * R], fxp = FXr[Ic[1]];
+          const T wup = r == 0 ? Wc[-WX] : ucur[r > 0 ? r - 1 : 0];
+          const T fym = r == 0 ? FX[T2 + Ic[-64] * R] : fyprev;
+          const T wdn = r == RY - 1 ? Wc[WX] : ucur[r < RY - 1 ? r + 1 : 0];
+          const int pdn = r == RY - 1 ? (int)Ic[64] : pcur[r < RY - 1 ? r + 1 : 0];
+          const T fyp = FXr[T2 + pdn];
+          fyprev = fyp;
+          const bool m = !interior;
+          T acc = 0, t;
+          t = add_rn(acc, mul_rn(fxm, sub_rn(uc, Wc[-1])));
+          acc = (!m || i > 0) ? t : acc;
+          t = sub_rn(acc, mul_rn(fxp, sub_rn(Wc[1], uc)));
+          acc = (!m || i + 1 < N) ? t : acc;
+          t = add_rn(acc, mul_rn(fym, sub_rn(uc, wup)));
+          acc = (!m || j > 0) ? t : acc;
+          t = sub_rn(acc, mul_rn(fyp, sub_rn(wdn, uc)));
+          acc = (!m || j + 1 < N) ? t : acc;
+          if (kg0 + k > 0) acc = add_rn(acc, mul_rn(fzm[r], sub_rn(uc, um[r])));
+          const T un = (&nx_.W[0][0])[wo + WX * r];
+          const int pn = (&nx_.I[0][0])[io + 64 * r];
+          T fzp = 0;
+          if (hasp) {
+            fzp = FXr[2 * T2 + pn];
+            acc = sub_rn(acc, mul_rn(fzp, sub_rn(un, uc)));
+          }
+          if (kg0 + k == 0) acc = add_rn(acc, mul_rn(FT[3 * T2 + pc], uc));
+          if (kg0 + k == nzg - 1) acc = add_rn(acc, mul_rn(FT[3 * T2 + pc], uc));
+          qout[(long long)k * P + (long long)j * N + i] = acc;
+          if (PCG) {
+            const double a_ = acc, u_ = uc;
+            dqw = fma(a_, u_, dqw);
+            dqq = fma(a_, a_, dqq);
+            dww = fma(u_, u_, dww);
+          }
+          unext[r] = un;
+          pnext[r] = pn;
+          um[r] = uc;
+          fzm[r] = fzp;
+        }
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          ucur[r] = unext[r];
+          pcur[r] = pnext[r];
+        }
+        continue;
       }
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
-        const int j = j0 + ly + 8 * r;
-        const int w_ = wo + 8 * WX * r, i_ = io + 8 * 64 * r;
+        const int j = j0 + ly0 + rs * r;
+        const int w_ = wo + rs * WX * r, i_ = io + rs * 64 * r;
         const T uc = ucur[r];
         const int pc = pcur[r];
         T fzp;

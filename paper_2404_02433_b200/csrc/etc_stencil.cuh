@@ -615,6 +615,9 @@ __global__ void __launch_bounds__(256, 4)
         constexpr int R = PH_RS;
         T unext[RY];
         int pnext[RY];
+        // the plane's rows; MASK (edge blocks only) applies the boundary masks
+        auto rows = [&](auto mk) {
+        constexpr bool MASK = decltype(mk)::value;
         T fyprev = 0;
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
@@ -632,16 +635,15 @@ __global__ void __launch_bounds__(256, 4)
           const int pdn = r == RY - 1 ? (int)Ic[64] : pcur[r < RY - 1 ? r + 1 : 0];
           const T fyp = FXr[T2 + pdn];
           fyprev = fyp;
-          const bool m = !interior;
           T acc = 0, t;
           t = add_rn(acc, mul_rn(fxm, sub_rn(uc, Wc[-1])));
-          acc = (!m || i > 0) ? t : acc;
+          acc = (!MASK || i > 0) ? t : acc;
           t = sub_rn(acc, mul_rn(fxp, sub_rn(Wc[1], uc)));
-          acc = (!m || i + 1 < N) ? t : acc;
+          acc = (!MASK || i + 1 < N) ? t : acc;
           t = add_rn(acc, mul_rn(fym, sub_rn(uc, wup)));
-          acc = (!m || j > 0) ? t : acc;
+          acc = (!MASK || j > 0) ? t : acc;
           t = sub_rn(acc, mul_rn(fyp, sub_rn(wdn, uc)));
-          acc = (!m || j + 1 < N) ? t : acc;
+          acc = (!MASK || j + 1 < N) ? t : acc;
           if (kg0 + k > 0) acc = add_rn(acc, mul_rn(fzm[r], sub_rn(uc, um[r])));
           const T un = (&nx_.W[0][0])[wo + WX * r];
           const int pn = (&nx_.I[0][0])[io + 64 * r];
@@ -664,6 +666,11 @@ __global__ void __launch_bounds__(256, 4)
           um[r] = uc;
           fzm[r] = fzp;
         }
+        };
+        if (interior)
+          rows(std::false_type{});
+        else
+          rows(std::true_type{});
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
           ucur[r] = unext[r];

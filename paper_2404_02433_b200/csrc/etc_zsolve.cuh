@@ -218,7 +218,22 @@ __global__ void __launch_bounds__(TC * 32 + 32, 1)
       // reciprocal pivots straight from the table (rows L-1 of the last block
       // continue the interior table); values in registers
       const R* rp = (q == 0) ? &Tt.rf[0][c] : &Tt.ri[0][c];
-      auto rcp = [&](int i) -> R { return rp[i * TC]; };
+      // float: the block's reciprocal pivots fit in registers, read once per
+      // tile instead of once per sweep (0.340 -> 0.326 ms at 512^3); double
+      // keeps them in the table (in registers they spill at the 96-register
+      // cap of the 544-thread CTA: 0.451 -> 0.594 ms)
+      constexpr bool RREG = sizeof(R) == 4;
+      R rcpv[RREG ? L : 1];
+      if constexpr (RREG) {
+#pragma unroll
+        for (int i = 0; i < L; ++i) rcpv[i] = (i < L - 1 || last) ? rp[i * TC] : (R)0;
+      }
+      auto rcp = [&](int i) -> R {
+        if constexpr (RREG)
+          return rcpv[i];
+        else
+          return rp[i * TC];
+      };
       R my[L];
       mbar_wait(&bar[s], (unsigned)((n / S) & 1));
       // local forward elimination; rows 0..L-2 in every block, row L-1 only in the last
